@@ -1,0 +1,124 @@
+/*
+ * delimit.h -- C ABI of libdelimit_sm100a.so, the B200 (sm_100a) kernels behind
+ * the Signal2SH -> LocalSphericalConvolution -> SH2Signal path.
+ *
+ * Every entry point takes raw DEVICE pointers to float32 buffers, int64 sizes
+ * and a cudaStream_t (passed as void*), enqueues work on that stream only and
+ * returns 0 on success or a DL_E* code; dl_last_error() then holds a message.
+ * The library never allocates device memory: callers own outputs and
+ * workspaces (sizes from the *_workspace_bytes queries).  There is no CPU
+ * fallback: with no usable sm_100a device every compute entry returns
+ * DL_ENODEVICE.
+ *
+ * Volume layout (the reference's 5-D contract, fitting.py:33-89):
+ *   (subjects, shells * C, X, Y, Z) C-contiguous; shell s owns channels
+ *   [s*C, (s+1)*C); nvox = X*Y*Z voxels are contiguous per channel.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/sphdwi/):
+ *   dl_chan_contract_f32    <- fitting._apply_channel_matrix  fitting.py:155-188
+ *                              (and thus signal_to_sh fitting.py:206-236,
+ *                               sh_to_signal fitting.py:239-250, the LSC refit lsc.py:197)
+ *   dl_lsc_build_operator_f32, dl_lsc_forward via dl_chan_contract_f32
+ *                           <- _kernels.lsc_combine _kernels.py:187-206 + refit lsc.py:194-198
+ *   dl_lsc_wgrad_f32        <- (no reference counterpart: backward is out of the
+ *                               reference's scope)
+ *   dl_chain_fwd_f32 / dl_chain_bwd_f32
+ *                           <- signal_to_sh -> lsc_forward -> sh_to_signal as the
+ *                              CLI chains them (cli.py:159-245), fused.
+ */
+#ifndef DELIMIT_H_
+#define DELIMIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DL_OK = 0,
+  DL_EINVAL = 1,       /* bad argument (shape, null pointer, alignment) */
+  DL_ECUDA = 2,        /* CUDA runtime / launch error */
+  DL_ENODEVICE = 3,    /* no sm_100a device available */
+};
+
+/* ABI version (major*100 + minor). */
+int dl_abi_version(void);
+/* Message for the last non-zero status returned on this host thread. */
+const char* dl_last_error(void);
+/* 1 if the current CUDA device is sm_100 (B200), else 0 (sets dl_last_error). */
+int dl_device_supported(void);
+
+/*
+ * Per-voxel channel contraction with optional bias:
+ *   out[b, g*c_out + i, v] = bias_g[i] + sum_j W_g[i, j] * in[b, g*c_in + j, v]
+ * W is row-major (c_out, c_in); with w_per_group != 0 W holds `groups`
+ * consecutive matrices (and bias `groups` consecutive vectors), else one
+ * matrix is shared by every group.  bias may be NULL.  in_bs / out_bs are the
+ * subject strides in elements.  in and out must not alias.
+ * Replaces fitting._apply_channel_matrix (fitting.py:155-188); groups = shells.
+ */
+int dl_chan_contract_f32(const float* in, float* out, const float* W, const float* bias,
+                         int64_t nbatch, int64_t groups, int64_t c_in, int64_t c_out,
+                         int64_t nvox, int64_t in_bs, int64_t out_bs, int w_per_group,
+                         void* stream);
+
+/*
+ * Folded LSC operator from the kernel parameters:
+ *   L[o*r_out + r, s*r_in + t]  = sum_k w[o, s, k] * P[k, r, t]
+ *   Lt = L^T,  bvec[o*r_out + r] = bias[o] * beta[r]
+ * P_k = refit . resample[k::K] (K, r_out, r_in), beta = refit . 1 (r_out).
+ * w is (s_out, s_in, K) (the .sconv.weight (s_out, s_in, 1, K) memory).
+ * L, Lt: (s_out*r_out) x (s_in*r_in) resp. transposed; bvec: s_out*r_out.
+ * Equivalent to lsc_combine + refit (_kernels.py:91-104, lsc.py:197) in exact arithmetic.
+ */
+int dl_lsc_build_operator_f32(const float* P, const float* beta, const float* w, const float* bias,
+                              float* L, float* Lt, float* bvec, int64_t s_out, int64_t s_in,
+                              int64_t K, int64_t r_out, int64_t r_in, void* stream);
+
+/*
+ * LSC weight/bias gradient.  With g = dL/dc_out (nbatch, s_out*r_out, nvox)
+ * and c = c_in (nbatch, s_in*r_in, nvox):
+ *   G      = sum_{b,v} g[b,:,v] c[b,:,v]^T          ((s_out r_out) x (s_in r_in))
+ *   dW[o,s,k] = <P_k, G_{o,s}>_F,   db[o] = beta . sum_{b,v} g[b, o*r_out:(o+1)*r_out, v]
+ * Deterministic (fixed partition + fixed-order float64 reduction).
+ * workspace: dl_lsc_wgrad_workspace_bytes() bytes of device memory.
+ */
+size_t dl_lsc_wgrad_workspace_bytes(int64_t s_out, int64_t s_in, int64_t r_out, int64_t r_in);
+int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float* beta,
+                     float* dW, float* db, void* workspace, int64_t nbatch, int64_t s_out,
+                     int64_t s_in, int64_t K, int64_t r_out, int64_t r_in, int64_t nvox,
+                     int64_t g_bs, int64_t c_bs, void* stream);
+
+/*
+ * Fused chain Signal2SH (M: r x n per input shell, shared or per shell)
+ *   -> LSC (L, bvec from dl_lsc_build_operator_f32)
+ *   -> SH2Signal (Bt: n_out x r_out shared by the output shells).
+ * x: (nbatch, s_in*n, nvox) -> y: (nbatch, s_out*n_out, nvox).
+ * Backward: dy -> dx (may be NULL) and the LSC gradient (dW, db; may be NULL).
+ * M_t / Bt_t are the transposed matrices (n x r per shell, r_out x n_out).
+ * workspace: dl_chain_workspace_bytes() bytes.
+ */
+size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
+                                int64_t r_out, int64_t n_out, int64_t nvox);
+int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, const float* L,
+                     const float* bvec, const float* Bt, void* workspace, int64_t nbatch,
+                     int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out,
+                     int64_t n_out, int64_t nvox, void* stream);
+int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, float* db,
+                     const float* M, const float* M_t, int m_per_shell, const float* Lt,
+                     const float* Bt_t, const float* P, const float* beta, void* workspace,
+                     int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K, int64_t n,
+                     int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+
+/* Number of kernel launches the last call on this host thread enqueued. */
+int dl_last_launch_count(void);
+/* Kernel launches enqueued by this library since it was loaded (all threads). */
+int64_t dl_total_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DELIMIT_H_ */

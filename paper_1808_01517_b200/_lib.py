@@ -1,0 +1,83 @@
+"""ctypes binding of libdelimit_sm100a.so (the C ABI in include/delimit.h).
+
+The library is the only compute path: if it is missing or the device is not
+sm_100a every op raises DeviceError.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import DeviceError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdelimit_sm100a.so")
+
+_c_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_size = ctypes.c_size_t
+
+# name -> (restype, argtypes); must match include/delimit.h
+SIGNATURES = {
+    "dl_abi_version": (_int, []),
+    "dl_last_error": (ctypes.c_char_p, []),
+    "dl_device_supported": (_int, []),
+    "dl_last_launch_count": (_int, []),
+    "dl_total_launch_count": (_i64, []),
+    "dl_chan_contract_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _c_p]),
+    "dl_lsc_build_operator_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _i64, _c_p]),
+    "dl_lsc_wgrad_workspace_bytes": (_size, [_i64, _i64, _i64, _i64]),
+    "dl_lsc_wgrad_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _i64, _i64,
+                                _i64, _i64, _i64, _c_p]),
+    "dl_chain_workspace_bytes": (_size, [_i64] * 8),
+    "dl_chain_fwd_f32": (_int, [_c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p, _c_p] + [_i64] * 8 + [_c_p]),
+    "dl_chain_bwd_f32": (_int, [_c_p] * 6 + [_c_p, _int, _c_p, _c_p, _c_p, _c_p, _c_p] + [_i64] * 9 + [_c_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the library.  Raises DeviceError if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise DeviceError(f"{os.path.basename(path)} is not built (run __graft_entry__.build()); "
+                                  "the sm_100a CUDA path is the only implementation")
+            lib = ctypes.CDLL(path)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().dl_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        raise DeviceError(f"{what}: {last_error()} (status {status})")
+
+
+def call(name: str, *args) -> None:
+    """Call a status-returning entry point and raise DeviceError on failure."""
+    check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().dl_last_launch_count())
+
+
+def total_launches() -> int:
+    """Kernel launches this library has enqueued since load (for bench.py's gpu_launches)."""
+    return int(load().dl_total_launch_count())

@@ -1,0 +1,30 @@
+"""Exception types, mirroring the reference's taxonomy (sphdwi/errors.py:8-45).
+
+The same conditions raise the same classes as the reference: channel / order /
+shell mismatches -> ShapeError, kernel length mismatch -> KernelMismatchError,
+ill-posed fits -> IllPosedFitError, bad scalar arguments -> ValueError.
+DeviceError is new: the path is CUDA-only and fails loudly without it.
+"""
+
+
+class SphdwiError(Exception):
+    """Base class for all package-specific errors (reference name kept for drop-in use)."""
+
+
+DelimitError = SphdwiError
+
+
+class ShapeError(SphdwiError):
+    """An array does not have the channel/volume layout an operation expects."""
+
+
+class IllPosedFitError(SphdwiError):
+    """The least-squares system is underdetermined or numerically rank deficient."""
+
+
+class KernelMismatchError(SphdwiError):
+    """A convolution kernel does not match the geometry it is applied with."""
+
+
+class DeviceError(SphdwiError, RuntimeError):
+    """No sm_100a device, missing CUDA library, or a CUDA error from the kernels."""

@@ -1,0 +1,190 @@
+"""Device ops over the C ABI, with autograd.
+
+Every op takes fp32 CUDA tensors in the reference's 5-D layout
+(subjects, shells*C, X, Y, Z) and enqueues sm_100a kernels on the current
+torch stream.  Non-CUDA input raises DeviceError: there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import DeviceError, ShapeError
+
+_NULL = ctypes.c_void_p(0)
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t) -> ctypes.c_void_p:
+    return _NULL if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def as_device_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    """fp32, contiguous, CUDA -- or DeviceError (no CPU fallback)."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise DeviceError(f"{name} must be a CUDA tensor on an sm_100a device; this implementation has no CPU path")
+    if t.dtype != torch.float32:
+        t = t.float()
+    return t.contiguous()
+
+
+def nvox_of(x: torch.Tensor) -> int:
+    n = 1
+    for d in x.shape[2:]:
+        n *= int(d)
+    return n
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ----------------------------------------------------------------------------- raw launchers
+def contract(x: torch.Tensor, W: torch.Tensor, c_in: int, c_out: int, groups: int, per_group: bool,
+             bias: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[b, g*c_out+i, v] = bias_g[i] + sum_j W_g[i,j] x[b, g*c_in+j, v]  (dl_chan_contract_f32)."""
+    B = x.shape[0]
+    if x.shape[1] != groups * c_in:
+        raise ShapeError(f"expected {groups * c_in} channels, got {x.shape[1]}")
+    V = nvox_of(x)
+    if out is None:
+        out = torch.empty((B, groups * c_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
+    _lib.call("dl_chan_contract_f32", _p(x), _p(out), _p(W), _p(bias), B, groups, c_in, c_out, V,
+              groups * c_in * V, groups * c_out * V, int(per_group), _stream())
+    return out
+
+
+def build_lsc_operator(fold: torch.Tensor, beta: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None,
+                       want_L=True, want_Lt=True, want_bvec=True):
+    """(L, Lt, bvec) from the kernel parameters (dl_lsc_build_operator_f32)."""
+    K, r_out, r_in = fold.shape
+    s_out, s_in = weight.shape[0], weight.shape[1]
+    dev = weight.device
+    rows, cols = s_out * r_out, s_in * r_in
+    L = torch.empty((rows, cols), dtype=torch.float32, device=dev) if want_L else None
+    Lt = torch.empty((cols, rows), dtype=torch.float32, device=dev) if want_Lt else None
+    bvec = torch.empty((rows,), dtype=torch.float32, device=dev) if want_bvec else None
+    _lib.call("dl_lsc_build_operator_f32", _p(fold), _p(beta), _p(weight), _p(bias), _p(L), _p(Lt), _p(bvec),
+              s_out, s_in, K, r_out, r_in, _stream())
+    return L, Lt, bvec
+
+
+def lsc_wgrad(g: torch.Tensor, c: torch.Tensor, fold: torch.Tensor, beta: torch.Tensor, s_out: int, s_in: int,
+              want_dW=True, want_db=True):
+    """(dW (s_out, s_in, K), db (s_out,)) = LSC parameter gradient (dl_lsc_wgrad_f32)."""
+    K, r_out, r_in = fold.shape
+    B, V = c.shape[0], nvox_of(c)
+    dev = c.device
+    dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=dev) if want_dW else None
+    db = torch.empty((s_out,), dtype=torch.float32, device=dev) if want_db else None
+    ws = _workspace(_lib.load().dl_lsc_wgrad_workspace_bytes(s_out, s_in, r_out, r_in), dev)
+    _lib.call("dl_lsc_wgrad_f32", _p(g), _p(c), _p(fold), _p(beta), _p(dW), _p(db), _p(ws), B, s_out, s_in, K,
+              r_out, r_in, V, s_out * r_out * V, s_in * r_in * V, _stream())
+    return dW, db
+
+
+# ----------------------------------------------------------------------------- autograd
+class ChannelMap(torch.autograd.Function):
+    """Per-shell linear map x[s] -> W_s x[s] (Signal2SH: W=M, SH2Signal: W=B'); grad uses W^T."""
+
+    @staticmethod
+    def forward(ctx, x, W, Wt, c_in, c_out, groups, per_group):
+        ctx.save_for_backward(Wt)
+        ctx.dims = (c_in, c_out, groups, per_group)
+        return contract(x, W, c_in, c_out, groups, per_group)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (Wt,) = ctx.saved_tensors
+        c_in, c_out, groups, per_group = ctx.dims
+        gx = None
+        if ctx.needs_input_grad[0]:
+            gx = contract(as_device_f32(gy, "grad"), Wt, c_out, c_in, groups, per_group)
+        return gx, None, None, None, None, None, None
+
+
+class LscFunction(torch.autograd.Function):
+    """Folded LSC: c_out = L(w) c_in + bias*beta; grads dc = L^T g, dW = <P_k, G>, db = beta.sum g."""
+
+    @staticmethod
+    def forward(ctx, c, weight, bias, fold, beta):
+        s_out, s_in = weight.shape[0], weight.shape[1]
+        K, r_out, r_in = fold.shape
+        L, _, bvec = build_lsc_operator(fold, beta, weight, bias, want_Lt=False)
+        out = contract(c, L, s_in * r_in, s_out * r_out, 1, False, bias=bvec)
+        ctx.save_for_backward(c, weight, fold, beta)
+        ctx.has_bias = bias is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        c, weight, fold, beta = ctx.saved_tensors
+        s_out, s_in = weight.shape[0], weight.shape[1]
+        K, r_out, r_in = fold.shape
+        g = as_device_f32(g, "grad")
+        dc = dW = db = None
+        if ctx.needs_input_grad[0]:
+            _, Lt, _ = build_lsc_operator(fold, beta, weight, None, want_L=False, want_bvec=False)
+            dc = contract(g, Lt, s_out * r_out, s_in * r_in, 1, False)
+        want_w = ctx.needs_input_grad[1]
+        want_b = ctx.has_bias and ctx.needs_input_grad[2]
+        if want_w or want_b:
+            dW, db = lsc_wgrad(g, c, fold, beta, s_out, s_in, want_w, want_b)
+            if dW is not None:
+                dW = dW.view(weight.shape)
+        return dc, dW, db, None, None
+
+
+class ChainFunction(torch.autograd.Function):
+    """Fused Signal2SH -> LSC -> SH2Signal (dl_chain_fwd_f32 / dl_chain_bwd_f32)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, M, Mt, per_shell, fold, beta, Bt, Btt):
+        s_out, s_in = weight.shape[0], weight.shape[1]
+        K, r_out, r_in = fold.shape
+        n = M.shape[-1]
+        n_out = Bt.shape[0]
+        B, V = x.shape[0], nvox_of(x)
+        L, _, bvec = build_lsc_operator(fold, beta, weight, bias, want_Lt=False)
+        y = torch.empty((B, s_out * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
+        lib = _lib.load()
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
+        _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt), _p(ws),
+                  B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
+        ctx.save_for_backward(x, weight, M, Mt, fold, beta, Btt)
+        ctx.per_shell = per_shell
+        ctx.has_bias = bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, weight, M, Mt, fold, beta, Btt = ctx.saved_tensors
+        s_out, s_in = weight.shape[0], weight.shape[1]
+        K, r_out, r_in = fold.shape
+        n = M.shape[-1]
+        n_out = Btt.shape[1]
+        B, V = x.shape[0], nvox_of(x)
+        dy = as_device_f32(dy, "grad")
+        want_x = ctx.needs_input_grad[0]
+        want_w = ctx.needs_input_grad[1]
+        want_b = ctx.has_bias and ctx.needs_input_grad[2]
+        dx = torch.empty_like(x) if want_x else None
+        dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=x.device) if want_w else None
+        db = torch.empty((s_out,), dtype=torch.float32, device=x.device) if want_b else None
+        Lt = build_lsc_operator(fold, beta, weight, None, want_L=False, want_bvec=False)[1] if want_x else None
+        lib = _lib.load()
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
+        _lib.call("dl_chain_bwd_f32", _p(x), _p(dy), _p(dx), _p(dW), _p(db), _p(M), _p(Mt), int(ctx.per_shell),
+                  _p(Lt), _p(Btt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out, n_out, V,
+                  _stream())
+        if dW is not None:
+            dW = dW.view(weight.shape)
+        return dx, dW, db, None, None, None, None, None, None, None

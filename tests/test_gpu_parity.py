@@ -1,0 +1,367 @@
+"""Parity of the sm_100a path against the reference (golden vectors) and the CPU oracle.
+
+Tolerances (north_star, stated per test): normwise max relative error
+max|got - ref| / max|ref| <= 1e-5 for Signal2SH / SH2Signal outputs and their
+adjoints, <= 1e-4 for LSC forward, LSC gradients and the fused chain.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1808_01517_b200 as dl
+from paper_1808_01517_b200 import functional as F
+from paper_1808_01517_b200.directions import unit_sphere_directions
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+TOL_SH = 1e-5
+TOL_LSC = 1e-4
+TWO_SQRT_PI = 2.0 * np.sqrt(np.pi)
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1808_01517_b200._build import build_library
+
+    build_library()
+    return torch.device("cuda:0")
+
+
+def T(a, dev, grad=False):
+    return torch.tensor(np.asarray(a), dtype=torch.float32, device=dev, requires_grad=grad)
+
+
+def N(t):
+    return t.detach().double().cpu().numpy()
+
+
+def rel(got, ref):
+    return port.rel_err(N(got) if isinstance(got, torch.Tensor) else got, ref)
+
+
+def make_lsc(dirs, si, so, oi, oo, sizes, alpha, lam, w, b, dev):
+    m = dl.LocalSphericalConvolution(si, so, oi, oo, dirs, sizes, lb_lambda=lam, angular_distance=alpha).to(dev)
+    m.load_kernel(dl.LscKernel(w, b))
+    return m
+
+
+# ------------------------------------------------------------------ Signal2SH / SH2Signal vs reference
+def test_signal2sh_matches_reference(golden, dev):
+    s2sh = dl.Signal2SH(8, golden["dirs90"], lb_lambda=0.006).to(dev)
+    x = T(golden["s2sh_x"], dev, grad=True)
+    c = s2sh(x)
+    assert tuple(c.shape) == (2, 135, 4, 4, 4)
+    assert rel(c, golden["s2sh_c"]) <= TOL_SH
+    c.backward(T(golden["s2sh_dc"], dev))
+    assert rel(x.grad, golden["s2sh_dx"]) <= TOL_SH
+
+
+def test_signal2sh_per_shell_operators(golden, dev):
+    tables = np.stack([golden["dirs30"], golden["pershell_dirs_b"]])
+    s2sh = dl.Signal2SH(4, tables, lb_lambda=0.006).to(dev)
+    assert rel(s2sh(T(golden["pershell_x"], dev)), golden["pershell_c"]) <= TOL_SH
+
+
+@pytest.mark.parametrize("target,key", [("dirs90", "sh2s_y90"), ("sh2s_target60", "sh2s_y60")])
+def test_sh2signal_matches_reference(golden, dev, target, key):
+    sh2s = dl.SH2Signal(8, golden[target]).to(dev)
+    c = T(golden["sh2s_c"], dev, grad=True)
+    y = sh2s(c)
+    assert rel(y, golden[key]) <= TOL_SH
+    if target == "dirs90":
+        y.backward(T(golden["sh2s_dy"], dev))
+        assert rel(c.grad, golden["sh2s_dc"]) <= TOL_SH
+
+
+# ------------------------------------------------------------------ LSC vs reference
+LSC_CASES = [  # tag, dirs, S_in, S_out, order_in, order_out, sizes, alpha, lambda
+    ("lsc33", "dirs90", 3, 3, 8, 8, [5], np.pi / 5, 0.006),
+    ("lsc32", "dirs90", 3, 2, 8, 8, [5], np.pi / 5, 0.006),
+    ("lsc11", "dirs90", 1, 1, 8, 8, [5], np.pi / 5, 0.006),
+    ("lscr2", "dirs30", 1, 1, 4, 4, [4, 8], 0.35, 0.0),
+    ("lsco42", "dirs30", 1, 1, 4, 2, [5], 0.52, 0.0),
+]
+
+
+@pytest.mark.parametrize("tag,dirs,si,so,oi,oo,sizes,alpha,lam", LSC_CASES)
+def test_lsc_forward_backward_match_reference(golden, dev, tag, dirs, si, so, oi, oo, sizes, alpha, lam):
+    lsc = make_lsc(golden[dirs], si, so, oi, oo, sizes, alpha, lam, golden[f"{tag}_w"], golden[f"{tag}_b"], dev)
+    c = T(golden[f"{tag}_c"], dev, grad=True)
+    u = lsc(c)
+    assert rel(u, golden[f"{tag}_u"]) <= TOL_LSC
+    u.backward(T(golden[f"{tag}_g"], dev))
+    assert rel(c.grad, golden[f"{tag}_dc"]) <= TOL_LSC
+    assert rel(lsc.sconv.weight.grad[:, :, 0, :], golden[f"{tag}_dW"]) <= TOL_LSC
+    assert rel(lsc.sconv.bias.grad, golden[f"{tag}_db"]) <= TOL_LSC
+
+
+# ------------------------------------------------------------------ fused chain vs reference
+def chain_modules(golden, dev, w=None, b=None, lam=0.006):
+    d = golden["dirs90"]
+    s2sh = dl.Signal2SH(8, d, lb_lambda=lam).to(dev)
+    lsc = make_lsc(d, 3, 3, 8, 8, [5], np.pi / 5, lam, golden["chain_w"] if w is None else w,
+                   golden["chain_b"] if b is None else b, dev)
+    sh2s = dl.SH2Signal(8, d).to(dev)
+    return s2sh, lsc, sh2s
+
+
+def test_chain_matches_reference(golden, dev):
+    s2sh, lsc, sh2s = chain_modules(golden, dev)
+    chain = dl.SphericalChain(s2sh, lsc, sh2s)
+    x = T(golden["s2sh_x"], dev, grad=True)
+    y = chain(x)
+    assert rel(y, golden["chain_y"]) <= TOL_LSC
+    y.backward(T(golden["chain_dy"], dev))
+    assert rel(x.grad, golden["chain_dx"]) <= TOL_LSC
+    assert rel(lsc.sconv.weight.grad[:, :, 0, :], golden["chain_dW"]) <= TOL_LSC
+    assert rel(lsc.sconv.bias.grad, golden["chain_db"]) <= TOL_LSC
+
+
+def test_chain_equals_module_composition(golden, dev):
+    s2sh, lsc, sh2s = chain_modules(golden, dev)
+    x1 = T(golden["s2sh_x"], dev, grad=True)
+    x2 = T(golden["s2sh_x"], dev, grad=True)
+    dy = T(golden["chain_dy"], dev)
+    y1 = dl.SphericalChain(s2sh, lsc, sh2s)(x1)
+    y1.backward(dy)
+    g1 = (x1.grad.clone(), lsc.sconv.weight.grad.clone(), lsc.sconv.bias.grad.clone())
+    lsc.zero_grad()
+    y2 = sh2s(lsc(s2sh(x2)))
+    y2.backward(dy)
+    assert rel(y1, N(y2)) <= 1e-5
+    assert rel(g1[0], N(x2.grad)) <= 1e-5
+    assert rel(g1[1], N(lsc.sconv.weight.grad)) <= 1e-5
+    assert rel(g1[2], N(lsc.sconv.bias.grad)) <= 1e-5
+
+
+# ------------------------------------------------------------------ functional drop-in API
+def test_functional_api(golden, dev):
+    d = golden["dirs90"]
+    op = dl.make_fit_operator(d, 8, 0.006)
+    vol = F.DwiVolume(T(golden["s2sh_x"], dev), shells=3)
+    sh = F.signal_to_sh(vol, op)
+    assert sh.shells == 3 and rel(sh.data, golden["s2sh_c"]) <= TOL_SH
+    back = F.sh_to_signal(F.ShVolume(T(golden["sh2s_c"], dev), dl.ShBasisSpec(8), 3), golden["sh2s_target60"])
+    assert rel(back.data, golden["sh2s_y60"]) <= TOL_SH
+    geom = dl.build_lsc_geometry(d, [5], np.pi / 5, 8, 8, 0.006)
+    out = F.lsc_forward(F.ShVolume(T(golden["lsc32_c"], dev), dl.ShBasisSpec(8), 3),
+                        dl.LscKernel(golden["lsc32_w"], golden["lsc32_b"]), geom)
+    assert out.shells == 2 and rel(out.data, golden["lsc32_u"]) <= TOL_LSC
+    # kernel seam: apply_channel_matrix / lsc_combine vs the oracle's restatements
+    rng = np.random.default_rng(3)
+    st = rng.normal(size=(2, 3, 90, 1500))
+    W = rng.normal(size=(45, 90))
+    got = F.apply_channel_matrix(W, T(st, dev))
+    assert rel(got, port.apply_channel_matrix(W, np.asarray(st, np.float32).astype(np.float64))) <= TOL_SH
+    w = rng.normal(size=(2, 3, 6))
+    b = rng.normal(size=2)
+    coeffs = np.asarray(rng.normal(size=(3, 45, 777)), np.float32).astype(np.float64)
+    got = F.lsc_combine(geom.resample_matrix, w, b, T(coeffs, dev))
+    assert tuple(got.shape) == (2, 90, 777)
+    assert rel(got, port.lsc_combine(geom.resample_matrix, w, b, coeffs)) <= TOL_LSC
+
+
+def test_functional_errors(golden, dev):
+    geom = dl.build_lsc_geometry(golden["dirs30"], [5], np.pi / 5, 4, 4, 0.0)
+    sh = F.ShVolume(torch.zeros(1, 6, 3, 1, 1, device=dev), dl.ShBasisSpec(2))
+    with pytest.raises(dl.ShapeError, match="order"):
+        F.lsc_forward(sh, dl.make_moving_average_kernel([5]), geom)
+    sh4 = F.ShVolume(torch.zeros(1, 15, 3, 1, 1, device=dev), dl.ShBasisSpec(4))
+    with pytest.raises(dl.KernelMismatchError, match="4.*6|6.*4"):
+        F.lsc_forward(sh4, dl.make_moving_average_kernel([3]), geom)
+    with pytest.raises(dl.ShapeError, match="shell"):
+        F.lsc_forward(sh4, dl.make_moving_average_kernel([5], shells_in=2), geom)
+    with pytest.raises(dl.ShapeError, match="expected"):
+        F.signal_to_sh(F.DwiVolume(torch.ones(1, 29, 2, 2, 2, device=dev)), dl.make_fit_operator(golden["dirs30"], 4))
+    with pytest.raises(dl.ShapeError, match="non-finite"):
+        F.DwiVolume(torch.full((1, 30, 1, 1, 1), float("nan"), device=dev))
+
+
+# ------------------------------------------------------------------ reference KATs through the fp32 modules
+def test_kat_constant_signal(dev):
+    d = unit_sphere_directions(30)
+    for lam in (0.0, 0.006, 0.06):   # pkg/tests/test_fitting.py:72-79
+        c = N(dl.Signal2SH(4, d, lb_lambda=lam).to(dev)(torch.ones(1, 30, 3, 2, 1, device=dev)))
+        assert np.max(np.abs(c[0, 0] - TWO_SQRT_PI)) <= 1e-5 and np.max(np.abs(c[0, 1:])) <= 1e-5
+    y = N(dl.SH2Signal(4, unit_sphere_directions(60)).to(dev)(
+        torch.tensor(np.eye(15)[0] * TWO_SQRT_PI, dtype=torch.float32, device=dev).view(1, 15, 1, 1, 1).expand(
+            1, 15, 2, 2, 2).contiguous()))
+    assert np.max(np.abs(y - 1.0)) <= 1e-5    # pkg/tests/test_fitting.py:176-181
+
+
+def test_kat_lsc_moving_average_identity_bias(dev, rng):
+    d = unit_sphere_directions(30)
+    ma = make_lsc(d, 1, 1, 4, 4, [5], np.pi / 5, 0.0, np.full((1, 1, 6), 1 / 6), np.zeros(1), dev)
+    const = np.zeros((1, 15, 4, 1, 1))
+    const[0, 0] = TWO_SQRT_PI
+    assert np.max(np.abs(N(ma(T(const, dev))) - const)) <= 1e-5          # test_lsc.py:99-107
+    ident = make_lsc(d, 1, 1, 4, 4, [5], np.pi / 5, 0.0, np.eye(6)[0].reshape(1, 1, 6), np.zeros(1), dev)
+    c = rng.normal(size=(1, 15, 25, 1, 1)) * 0.2
+    c[0, 0] = TWO_SQRT_PI
+    assert rel(ident(T(c, dev)), c) <= 1e-5                              # test_lsc.py:109-115
+    base = N(ma(T(c, dev)))
+    shifted = make_lsc(d, 1, 1, 4, 4, [5], np.pi / 5, 0.0, np.full((1, 1, 6), 1 / 6), np.array([0.37]), dev)
+    diff = N(shifted(T(c, dev))) - base
+    assert np.max(np.abs(diff[0, 0] - 0.37 * TWO_SQRT_PI)) <= 1e-5       # test_lsc.py:155-168
+    assert np.max(np.abs(diff[0, 1:])) <= 1e-5
+    out = N(ma(T(c, dev)))
+    fi = dl.high_degree_energy_fraction(c[0].reshape(15, -1), 4)
+    fo = dl.high_degree_energy_fraction(out[0].reshape(15, -1), 4)
+    assert np.all(fo <= fi + 1e-6)                                       # test_lsc.py:117-125
+
+
+def test_kat_zero_cross_shell_weights(dev, rng):
+    d = unit_sphere_directions(30)
+    w = rng.normal(size=(1, 1, 6))
+    w2 = np.zeros((2, 2, 6))
+    w2[0, 0], w2[1, 1] = w[0, 0], 2 * w[0, 0]
+    two = make_lsc(d, 2, 2, 4, 4, [5], np.pi / 5, 0.0, w2, np.zeros(2), dev)
+    one = make_lsc(d, 1, 1, 4, 4, [5], np.pi / 5, 0.0, w, np.zeros(1), dev)
+    c = T(rng.normal(size=(1, 30, 13, 1, 1)), dev)
+    assert rel(two(c)[:, :15], N(one(c[:, :15].contiguous()))) <= 1e-5  # test_lsc.py:170-183
+
+
+def test_subjects_independent_and_linear(dev, rng):
+    d = unit_sphere_directions(90)
+    s2sh = dl.Signal2SH(8, d, lb_lambda=0.006).to(dev)
+    x = T(rng.normal(size=(3, 270, 5, 3, 2)) + 1.0, dev)
+    batch = s2sh(x)
+    for s in range(3):
+        assert torch.equal(batch[s:s + 1], s2sh(x[s:s + 1].contiguous()))
+    x2 = T(rng.normal(size=(3, 270, 5, 3, 2)), dev)
+    lin = N(s2sh(0.7 * x - 2.3 * x2)) - (0.7 * N(s2sh(x)) - 2.3 * N(s2sh(x2)))
+    assert np.max(np.abs(lin)) <= 1e-5 * np.max(np.abs(N(s2sh(x))))
+
+
+# ------------------------------------------------------------------ edge cases: ragged / odd / empty / layouts
+@pytest.mark.parametrize("grid", [(1, 1, 1), (3, 1, 1), (7, 5, 3), (17, 1, 31), (33, 17, 9), (2, 256, 1)])
+def test_ragged_voxel_counts(dev, rng, grid):
+    d = unit_sphere_directions(90)
+    M, _, _ = port.fit_operator(d, 8, 0.006)
+    s2sh = dl.Signal2SH(8, d, lb_lambda=0.006).to(dev)
+    x = np.asarray(rng.uniform(0.1, 1.5, size=(2, 180, *grid)), np.float32).astype(np.float64)
+    assert rel(s2sh(T(x, dev)), port.signal_to_sh(x, M, 2)) <= TOL_SH
+    Bt = port.eval_basis(d, 8)
+    c = np.asarray(rng.normal(size=(1, 90, *grid)), np.float32).astype(np.float64)
+    assert rel(dl.SH2Signal(8, d).to(dev)(T(c, dev)), port.sh_to_signal(c, Bt, 2)) <= TOL_SH
+
+
+def test_empty_inputs(dev):
+    d = unit_sphere_directions(90)
+    s2sh = dl.Signal2SH(8, d).to(dev)
+    assert tuple(s2sh(torch.empty(0, 90, 2, 2, 2, device=dev)).shape) == (0, 45, 2, 2, 2)
+    assert tuple(s2sh(torch.empty(1, 90, 0, 2, 2, device=dev)).shape) == (1, 45, 0, 2, 2)
+    lsc = dl.LocalSphericalConvolution(1, 1, 8, 8, d, [5]).to(dev)
+    c = torch.empty(0, 45, 2, 2, 2, device=dev, requires_grad=True)
+    u = lsc(c)
+    u.sum().backward()
+    assert torch.all(lsc.sconv.weight.grad == 0) and torch.all(lsc.sconv.bias.grad == 0)
+
+
+def test_layout_coercion(dev, rng):
+    d = unit_sphere_directions(30)
+    s2sh = dl.Signal2SH(4, d).to(dev)
+    x = rng.uniform(0.1, 1.0, size=(1, 4, 3, 2, 30))
+    xt = torch.tensor(x, dtype=torch.float64, device=dev).permute(0, 4, 1, 2, 3)   # non-contiguous float64
+    ref = s2sh(xt.float().contiguous())
+    assert torch.equal(s2sh(xt), ref)
+
+
+def test_large_channel_orders(dev, rng):
+    # order 10 (R = 66) and a 3-shell 3->2 LSC with order_out != order_in at odd voxel counts
+    d = unit_sphere_directions(90)
+    M, _, _ = port.fit_operator(d, 10, 0.006)
+    x = np.asarray(rng.uniform(0.1, 1.5, size=(1, 180, 11, 3, 1)), np.float32).astype(np.float64)
+    assert rel(dl.Signal2SH(10, d, lb_lambda=0.006).to(dev)(T(x, dev)), port.signal_to_sh(x, M, 2)) <= TOL_SH
+    geo = port.lsc_geometry(d, [4, 6], 0.3, 8, 6, 0.006)
+    w = rng.normal(size=(2, 3, 11)) / 33
+    b = rng.normal(size=2) * 0.1
+    lsc = make_lsc(d, 3, 2, 8, 6, [4, 6], 0.3, 0.006, w, b, dev)
+    c = np.asarray(rng.normal(size=(2, 135, 5, 3, 3)), np.float32).astype(np.float64)
+    ct = T(c, dev, grad=True)
+    u = lsc(ct)
+    assert rel(u, port.lsc_forward(c, w, b, geo)) <= TOL_LSC
+    g = np.asarray(rng.normal(size=u.shape), np.float32).astype(np.float64)
+    u.backward(T(g, dev))
+    dc, dW, db = port.lsc_backward(c, g, w, geo)
+    assert rel(ct.grad, dc) <= TOL_LSC
+    assert rel(lsc.sconv.weight.grad[:, :, 0, :], dW) <= TOL_LSC
+    assert rel(lsc.sconv.bias.grad, db) <= TOL_LSC
+
+
+# ------------------------------------------------------------------ determinism and graph capture
+def test_weight_grad_deterministic(dev, rng):
+    d = unit_sphere_directions(90)
+    lsc = dl.LocalSphericalConvolution(3, 3, 8, 8, d, [5]).to(dev)
+    c = T(rng.normal(size=(1, 135, 40, 40, 20)), dev)
+    g = T(rng.normal(size=(1, 135, 40, 40, 20)), dev)
+    outs = []
+    for _ in range(2):
+        lsc.zero_grad()
+        lsc(c).backward(g)
+        outs.append((lsc.sconv.weight.grad.clone(), lsc.sconv.bias.grad.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_chain_cuda_graph_capture(golden, dev):
+    s2sh, lsc, sh2s = chain_modules(golden, dev)
+    chain = dl.SphericalChain(s2sh, lsc, sh2s)
+    x = T(golden["s2sh_x"], dev, grad=True)
+    dy = T(golden["chain_dy"], dev)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            x.grad = None
+            lsc.zero_grad(set_to_none=True)
+            chain(x).backward(dy)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    x.grad = None
+    lsc.zero_grad(set_to_none=True)
+    with torch.cuda.graph(g):
+        y = chain(x)
+        y.backward(dy)
+    g.replay()
+    torch.cuda.synchronize()
+    assert rel(y, golden["chain_y"]) <= TOL_LSC
+    assert rel(x.grad, golden["chain_dx"]) <= TOL_LSC
+
+
+# ------------------------------------------------------------------ full-size properties (HCP-sized volume)
+@pytest.mark.parametrize("shape", [(1, 270, 145, 174, 145)])
+def test_hcp_chain_sampled_voxels(dev, shape):
+    """At the BASELINE size, check a random sample of voxels exactly against the oracle
+    (voxels are independent: fitting.py:223, lsc.py:194) plus a checksum identity."""
+    d = unit_sphere_directions(90)
+    torch.manual_seed(0)
+    s2sh = dl.Signal2SH(8, d, lb_lambda=0.006).to(dev)
+    lsc = dl.LocalSphericalConvolution(3, 3, 8, 8, d, [5]).to(dev)
+    sh2s = dl.SH2Signal(8, d).to(dev)
+    chain = dl.SphericalChain(s2sh, lsc, sh2s)
+    gen = torch.Generator(device=dev).manual_seed(1)
+    x = (torch.rand(shape, generator=gen, device=dev) + 0.2).requires_grad_(True)
+    dy = torch.randn(shape, generator=gen, device=dev)
+    y = chain(x)
+    y.backward(dy)
+    V = shape[2] * shape[3] * shape[4]
+    idx = torch.randint(0, V, (2048,), generator=gen, device=dev)
+    xs = N(x.detach().view(1, 270, V)[:, :, idx]).reshape(1, 270, -1, 1, 1)
+    dys = N(dy.view(1, 270, V)[:, :, idx]).reshape(1, 270, -1, 1, 1)
+    M, _, _ = port.fit_operator(d, 8, 0.006)
+    geo = port.lsc_geometry(d, [5], np.pi / 5, 8, 8, 0.006)
+    Bt = port.eval_basis(d, 8)
+    w = N(lsc.sconv.weight)[:, :, 0, :]
+    b = N(lsc.sconv.bias)
+    assert rel(N(y.detach().view(1, 270, V)[:, :, idx]).reshape(xs.shape), port.chain_forward(xs, M, geo, w, b, Bt, 3)) <= TOL_LSC
+    dx_ref, _, _ = port.chain_backward(xs, dys, M, geo, w, Bt, 3)
+    assert rel(N(x.grad.view(1, 270, V)[:, :, idx]).reshape(xs.shape), dx_ref) <= TOL_LSC
+    # <dy, y(x) - y(0)> == <dW, w> + <x, dx> ... linear-map identity: <dy, J x> = <J^T dy, x>
+    y0 = chain(torch.zeros(1, 270, 1, 1, 1, device=dev))             # bias response only
+    lhs = float(torch.sum(dy.double() * (y.detach().double() - y0.detach().double())))
+    rhs = float(torch.sum(x.grad.double() * x.detach().double()))
+    assert abs(lhs - rhs) <= 1e-4 * (abs(lhs) + abs(rhs))
