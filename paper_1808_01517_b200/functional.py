@@ -41,7 +41,7 @@ def _dev(device=None):
 
 
 def _const(a, device) -> torch.Tensor:
-    return torch.tensor(np.array(a, dtype=np.float64), dtype=torch.float32, device=device)
+    return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), dtype=torch.float32, device=device).contiguous()
 
 
 @dataclass(frozen=True)

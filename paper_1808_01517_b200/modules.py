@@ -33,7 +33,7 @@ from .geometry import (
 
 
 def _f32(a) -> torch.Tensor:
-    return torch.tensor(np.array(a, dtype=np.float64), dtype=torch.float32)
+    return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), dtype=torch.float32).contiguous()
 
 
 def _check_5d(x: torch.Tensor, what: str) -> None:

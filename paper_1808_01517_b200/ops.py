@@ -54,6 +54,10 @@ def contract(x: torch.Tensor, W: torch.Tensor, c_in: int, c_out: int, groups: in
     B = x.shape[0]
     if x.shape[1] != groups * c_in:
         raise ShapeError(f"expected {groups * c_in} channels, got {x.shape[1]}")
+    if not (x.is_contiguous() and W.is_contiguous() and (bias is None or bias.is_contiguous())):
+        raise ShapeError("contract: operands must be contiguous")
+    if W.numel() != (groups if per_group else 1) * c_out * c_in:
+        raise ShapeError(f"operator has {W.numel()} entries, expected {(groups if per_group else 1) * c_out * c_in}")
     V = nvox_of(x)
     if out is None:
         out = torch.empty((B, groups * c_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
