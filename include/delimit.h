@@ -92,14 +92,21 @@ int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float
                      int64_t g_bs, int64_t c_bs, void* stream);
 
 /*
- * Fused chain Signal2SH (M: r x n per input shell, shared or per shell)
- *   -> LSC (L, bvec from dl_lsc_build_operator_f32)
- *   -> SH2Signal (Bt: n_out x r_out shared by the output shells).
- * x: (nbatch, s_in*n, nvox) -> y: (nbatch, s_out*n_out, nvox).
- * Backward: dy -> dx (may be NULL) and the LSC gradient (dW, db; may be NULL).
- * M_t / Bt_t are the transposed matrices (n x r per shell, r_out x n_out).
- * workspace: dl_chain_workspace_bytes() bytes.
+ * Fused chain Signal2SH -> LSC -> SH2Signal on the 5th-generation tensor cores (tcgen05).
+ *   M:  r_in x n fit matrix, one per input shell (m_per_shell) or shared;
+ *   L:  (s_out*r_out) x (s_in*r_in) folded LSC operator, bvec its bias response
+ *       (dl_lsc_build_operator_f32); Bt: n_out x r_out SH basis at the output directions.
+ * x: (nbatch, s_in*n, nvox) -> y: (nbatch, s_out*n_out, nvox) in one kernel; the SH
+ * intermediates never reach HBM.  Every product is an fp32-accurate split product
+ * (each fp32 operand as DELIMIT_SPLIT_TERMS = 3 (default) or 2 bf16 terms, fp32 accumulation).
+ * Backward: dy -> dx (one kernel, the adjoint chain, may be skipped with dx = NULL) and
+ * the LSC parameter gradient dW (s_out, s_in, K), db (s_out) from a fused Gram kernel
+ * (g = B'^T dy and c = M x recomputed on the tensor cores) plus a float64 finalize.
+ * workspace: dl_chain_workspace_bytes() bytes.  dl_chain_supported() says whether the
+ * channel counts fit the kernels' TMEM/shared-memory plan (3 shells x order 8 x 90 dirs do).
  */
+int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out);
+int dl_chain_split_terms(void);
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);
 int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, const float* L,
@@ -107,10 +114,10 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
                      int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out,
                      int64_t n_out, int64_t nvox, void* stream);
 int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, float* db,
-                     const float* M, const float* M_t, int m_per_shell, const float* Lt,
-                     const float* Bt_t, const float* P, const float* beta, void* workspace,
-                     int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K, int64_t n,
-                     int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+                     const float* M, int m_per_shell, const float* L, const float* Bt,
+                     const float* P, const float* beta, void* workspace, int64_t nbatch,
+                     int64_t s_in, int64_t s_out, int64_t K, int64_t n, int64_t r_in,
+                     int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
 
 /* Number of kernel launches the last call on this host thread enqueued. */
 int dl_last_launch_count(void);

@@ -200,8 +200,10 @@ class LocalSphericalConvolution(nn.Module):
 class SphericalChain(nn.Module):
     """Signal2SH -> LocalSphericalConvolution -> SH2Signal as ONE fused op (forward + backward).
 
-    Equivalent to sh2s(lsc(s2sh(x))) -- the chain the reference CLI runs
-    (cli.py:159-245) -- with the LSC parameters shared with `lsc`.
+    Equivalent to sh2s(lsc(s2sh(x))) -- the chain the reference CLI runs (cli.py:159-245) --
+    with the LSC parameters shared with `lsc`.  The fused path runs the whole chain in one
+    tcgen05 kernel per direction (intermediates stay in TMEM); channel counts beyond the
+    kernels' TMEM/shared-memory plan run the three layers one after the other instead.
     """
 
     def __init__(self, s2sh: Signal2SH, lsc: LocalSphericalConvolution, sh2s: SH2Signal):
@@ -213,6 +215,13 @@ class SphericalChain(nn.Module):
         if s2sh.per_shell and len(s2sh.operators) != lsc.shells_in:
             raise ShapeError(f"Signal2SH has {len(s2sh.operators)} shell operators, LSC expects {lsc.shells_in}")
         self.s2sh, self.lsc, self.sh2s = s2sh, lsc, sh2s
+        self._fused = None
+
+    def fused(self) -> bool:
+        if self._fused is None:
+            self._fused = ops.chain_supported(self.lsc.shells_in, self.lsc.shells_out, self.s2sh.n_gradients,
+                                              self.lsc.r_in, self.lsc.r_out, self.sh2s.n_gradients)
+        return self._fused
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         _check_5d(x, "signal")
@@ -221,9 +230,11 @@ class SphericalChain(nn.Module):
             raise ShapeError(f"kernel expects {self.lsc.shells_in} input shells, volume has {s}")
         self.lsc._validate(torch.empty((1, s * self.lsc.r_in, 1, 1, 1), device="meta"))
         x = ops.as_device_f32(x, "signal")
+        if not self.fused():
+            return self.sh2s(self.lsc(self.s2sh(x)))
         w = self.lsc.sconv.weight
         w3 = w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous()
         b = self.lsc.sconv.bias
         return ops.ChainFunction.apply(x, w3, None if b is None else b.float().contiguous(),
-                                       self.s2sh.fit_matrix, self.s2sh.fit_matrix_t, self.s2sh.per_shell,
-                                       self.lsc.fold, self.lsc.beta, self.sh2s.basis, self.sh2s.basis_t)
+                                       self.s2sh.fit_matrix, self.s2sh.per_shell, self.lsc.fold, self.lsc.beta,
+                                       self.sh2s.basis)

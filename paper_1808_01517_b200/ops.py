@@ -148,10 +148,15 @@ class LscFunction(torch.autograd.Function):
 
 
 class ChainFunction(torch.autograd.Function):
-    """Fused Signal2SH -> LSC -> SH2Signal (dl_chain_fwd_f32 / dl_chain_bwd_f32)."""
+    """Fused Signal2SH -> LSC -> SH2Signal on tcgen05 (dl_chain_fwd_f32 / dl_chain_bwd_f32).
+
+    Forward is one kernel (x -> y).  Backward is one kernel for dx (the adjoint chain) and
+    one Gram kernel for the LSC parameters (+ a float64 finalize).  The intermediates never
+    touch HBM; x is kept for the weight gradient.
+    """
 
     @staticmethod
-    def forward(ctx, x, weight, bias, M, Mt, per_shell, fold, beta, Bt, Btt):
+    def forward(ctx, x, weight, bias, M, per_shell, fold, beta, Bt):
         s_out, s_in = weight.shape[0], weight.shape[1]
         K, r_out, r_in = fold.shape
         n = M.shape[-1]
@@ -163,18 +168,18 @@ class ChainFunction(torch.autograd.Function):
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
         _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt), _p(ws),
                   B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
-        ctx.save_for_backward(x, weight, M, Mt, fold, beta, Btt)
+        ctx.save_for_backward(x, weight, M, fold, beta, Bt, L)
         ctx.per_shell = per_shell
         ctx.has_bias = bias is not None
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x, weight, M, Mt, fold, beta, Btt = ctx.saved_tensors
+        x, weight, M, fold, beta, Bt, L = ctx.saved_tensors
         s_out, s_in = weight.shape[0], weight.shape[1]
         K, r_out, r_in = fold.shape
         n = M.shape[-1]
-        n_out = Btt.shape[1]
+        n_out = Bt.shape[0]
         B, V = x.shape[0], nvox_of(x)
         dy = as_device_f32(dy, "grad")
         want_x = ctx.needs_input_grad[0]
@@ -183,12 +188,17 @@ class ChainFunction(torch.autograd.Function):
         dx = torch.empty_like(x) if want_x else None
         dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=x.device) if want_w else None
         db = torch.empty((s_out,), dtype=torch.float32, device=x.device) if want_b else None
-        Lt = build_lsc_operator(fold, beta, weight, None, want_L=False, want_bvec=False)[1] if want_x else None
+        if dx is None and dW is None and db is None:
+            return None, None, None, None, None, None, None, None
         lib = _lib.load()
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
-        _lib.call("dl_chain_bwd_f32", _p(x), _p(dy), _p(dx), _p(dW), _p(db), _p(M), _p(Mt), int(ctx.per_shell),
-                  _p(Lt), _p(Btt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out, n_out, V,
-                  _stream())
+        _lib.call("dl_chain_bwd_f32", _p(x), _p(dy), _p(dx), _p(dW), _p(db), _p(M), int(ctx.per_shell), _p(L),
+                  _p(Bt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out, n_out, V, _stream())
         if dW is not None:
             dW = dW.view(weight.shape)
-        return dx, dW, db, None, None, None, None, None, None, None
+        return dx, dW, db, None, None, None, None, None
+
+
+def chain_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int) -> bool:
+    """True if the fused tcgen05 chain kernels fit these channel counts."""
+    return bool(_lib.load().dl_chain_supported(s_in, s_out, n, r_in, r_out, n_out))

@@ -365,3 +365,48 @@ def test_hcp_chain_sampled_voxels(dev, shape):
     lhs = float(torch.sum(dy.double() * (y.detach().double() - y0.detach().double())))
     rhs = float(torch.sum(x.grad.double() * x.detach().double()))
     assert abs(lhs - rhs) <= 1e-4 * (abs(lhs) + abs(rhs))
+
+
+# ------------------------------------------------------------------ fused tcgen05 chain across shapes
+CHAIN_CASES = [  # s_in, s_out, order_in, order_out, n_in, n_out, grid, per_shell
+    (3, 3, 8, 8, 90, 90, (4, 4, 4), False),
+    (3, 3, 8, 8, 90, 90, (7, 5, 3), False),      # one partial tile
+    (3, 3, 8, 8, 90, 90, (13, 11, 7), True),     # several tiles + tail, per-shell Signal2SH tables
+    (3, 2, 8, 8, 90, 60, (9, 9, 2), False),      # S_in != S_out, other output directions
+    (1, 1, 8, 8, 90, 90, (33, 1, 9), False),
+    (2, 3, 8, 6, 60, 30, (5, 5, 5), False),      # order_out != order_in
+    (1, 1, 4, 4, 30, 30, (3, 3, 3), False),
+]
+
+
+@pytest.mark.parametrize("si,so,oi,oo,ni,no,grid,per_shell", CHAIN_CASES)
+def test_fused_chain_vs_oracle(dev, si, so, oi, oo, ni, no, grid, per_shell):
+    rng = np.random.default_rng(hash((si, so, oi, oo, ni, no, grid)) % 2**32)
+    d_in = unit_sphere_directions(ni)
+    d_out = unit_sphere_directions(no)
+    tables = np.stack([d_in] + [rng.normal(size=(ni, 3)) for _ in range(si - 1)]) if per_shell else d_in
+    s2sh = dl.Signal2SH(oi, tables, lb_lambda=0.006).to(dev)
+    K = 6
+    w = rng.normal(size=(so, si, K)) / (si * K)
+    b = rng.normal(size=so) * 0.1
+    lsc = make_lsc(d_in, si, so, oi, oo, [5], np.pi / 5, 0.006, w, b, dev)
+    sh2s = dl.SH2Signal(oo, d_out).to(dev)
+    chain = dl.SphericalChain(s2sh, lsc, sh2s)
+    assert chain.fused()
+    B = 2
+    x = np.asarray(rng.uniform(0.1, 1.3, size=(B, si * ni, *grid)), np.float32).astype(np.float64)
+    dy = np.asarray(rng.normal(size=(B, so * no, *grid)), np.float32).astype(np.float64)
+    xt = T(x, dev, grad=True)
+    y = chain(xt)
+    y.backward(T(dy, dev))
+    Ms = [op.fit_matrix for op in s2sh.operators]
+    M = Ms if per_shell else Ms[0]
+    geo = port.lsc_geometry(d_in, [5], np.pi / 5, oi, oo, 0.006)
+    Bt = port.eval_basis(d_out, oo)
+    wq, bq = N(lsc.sconv.weight)[:, :, 0, :], N(lsc.sconv.bias)
+    y_ref = port.chain_forward(x, M, geo, wq, bq, Bt, si)
+    dx_ref, dW_ref, db_ref = port.chain_backward(x, dy, M, geo, wq, Bt, si)
+    assert rel(y, y_ref) <= TOL_LSC
+    assert rel(xt.grad, dx_ref) <= TOL_LSC
+    assert rel(lsc.sconv.weight.grad[:, :, 0, :], dW_ref) <= TOL_LSC
+    assert rel(lsc.sconv.bias.grad, db_ref) <= TOL_LSC
