@@ -105,7 +105,8 @@ int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float
  * workspace: dl_chain_workspace_bytes() bytes.  dl_chain_supported() says whether the
  * channel counts fit the kernels' TMEM/shared-memory plan (3 shells x order 8 x 90 dirs do).
  */
-int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out);
+int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                       int m_per_shell);
 int dl_chain_split_terms(void);
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);

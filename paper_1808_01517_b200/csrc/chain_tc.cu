@@ -743,14 +743,23 @@ bool plan_chain3(Chain3& p, int parts) {
   p.colD1 = A1;
   p.colA2 = A1 + D1;
   p.colD2 = 0;
-  p.colA3 = D2;
-  if (p.colA2 + A2 > 512 || D2 + A3 > (int)p.colA2 || D1 > 512) return false;
-  if ((int)p.colA2 + A2 + p.N3 <= 512) {
-    p.colD3 = p.colA2 + A2;
-    p.d3_sync = 0;
-  } else if (D2 + A3 + p.N3 <= 512) {
-    p.colD3 = D2 + A3;
-    p.d3_sync = 1;
+  // D2 reuses [0, ...) once stage 1 is drained; it must not overlap A2 (read by stage-2 MMAs).
+  if ((int)p.colA2 + A2 > 512 || D2 > (int)p.colA2 || D1 > 512) return false;
+  p.d3_sync = 0;
+  if (D2 + A3 <= (int)p.colA2) {
+    // A3 right after D2 (below A2); D3 after A2, or over A2 once all stage-2 MMAs completed
+    p.colA3 = D2;
+    if ((int)p.colA2 + A2 + p.N3 <= 512) {
+      p.colD3 = p.colA2 + A2;
+    } else if (D2 + A3 + p.N3 <= 512) {
+      p.colD3 = D2 + A3;
+      p.d3_sync = 1;
+    } else {
+      return false;
+    }
+  } else if ((int)p.colA2 + A2 + A3 + p.N3 <= 512) {
+    p.colA3 = p.colA2 + A2;  // both stage-3 buffers above A2
+    p.colD3 = p.colA3 + A3;
   } else {
     return false;
   }
@@ -910,10 +919,10 @@ int grid_for(int64_t ntiles, int sm) { return (int)(ntiles < sm ? (ntiles > 0 ? 
 
 extern "C" {
 
-int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out) {
+int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                       int m_per_shell) {
   using namespace dl::tc;
-  return chain_fits(make_dims(1, s_in, s_out, n, r_in, r_out, n_out, 1, 0)) &&
-         chain_fits(make_dims(1, s_in, s_out, n, r_in, r_out, n_out, 1, 1)) ? 1 : 0;
+  return chain_fits(make_dims(1, s_in, s_out, n, r_in, r_out, n_out, 1, m_per_shell)) ? 1 : 0;
 }
 
 int dl_chain_split_terms(void) { return dl::tc::split_terms(); }

@@ -220,7 +220,8 @@ class SphericalChain(nn.Module):
     def fused(self) -> bool:
         if self._fused is None:
             self._fused = ops.chain_supported(self.lsc.shells_in, self.lsc.shells_out, self.s2sh.n_gradients,
-                                              self.lsc.r_in, self.lsc.r_out, self.sh2s.n_gradients)
+                                              self.lsc.r_in, self.lsc.r_out, self.sh2s.n_gradients,
+                                              self.s2sh.per_shell)
         return self._fused
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:

@@ -199,6 +199,6 @@ class ChainFunction(torch.autograd.Function):
         return dx, dW, db, None, None, None, None, None
 
 
-def chain_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int) -> bool:
+def chain_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int, per_shell: bool) -> bool:
     """True if the fused tcgen05 chain kernels fit these channel counts."""
-    return bool(_lib.load().dl_chain_supported(s_in, s_out, n, r_in, r_out, n_out))
+    return bool(_lib.load().dl_chain_supported(s_in, s_out, n, r_in, r_out, n_out, int(per_shell)))

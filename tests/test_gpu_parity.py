@@ -371,7 +371,8 @@ def test_hcp_chain_sampled_voxels(dev, shape):
 CHAIN_CASES = [  # s_in, s_out, order_in, order_out, n_in, n_out, grid, per_shell
     (3, 3, 8, 8, 90, 90, (4, 4, 4), False),
     (3, 3, 8, 8, 90, 90, (7, 5, 3), False),      # one partial tile
-    (3, 3, 8, 8, 90, 90, (13, 11, 7), True),     # several tiles + tail, per-shell Signal2SH tables
+    (3, 3, 8, 8, 90, 90, (13, 11, 7), False),    # several tiles + tail
+    (2, 2, 8, 8, 90, 90, (13, 11, 7), True),     # per-shell Signal2SH tables
     (3, 2, 8, 8, 90, 60, (9, 9, 2), False),      # S_in != S_out, other output directions
     (1, 1, 8, 8, 90, 90, (33, 1, 9), False),
     (2, 3, 8, 6, 60, 30, (5, 5, 5), False),      # order_out != order_in
