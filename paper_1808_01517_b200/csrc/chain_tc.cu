@@ -50,6 +50,33 @@ __device__ __forceinline__ void pair_of(int parts, int idx, int& i, int& j) {
   }
 }
 
+// Compile-time (i, j) pair lists (activation term i, weight term j).
+template <int P> struct Pairs;
+template <> struct Pairs<3> {
+  static constexpr int n = 6;
+  __device__ static constexpr int i(int k) { return k == 0 ? 2 : k == 1 ? 1 : k == 2 ? 0 : k == 3 ? 1 : 0; }
+  __device__ static constexpr int j(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 0 : k == 4 ? 1 : 0; }
+};
+template <> struct Pairs<2> {
+  static constexpr int n = 3;
+  __device__ static constexpr int i(int k) { return k == 0 ? 1 : 0; }
+  __device__ static constexpr int j(int k) { return k == 1 ? 1 : 0; }
+};
+
+// Byte advance of a weight descriptor per K-step (added to the start-address field, >> 4).
+__device__ __forceinline__ uint64_t wkstep(int cols, int kmajor) {
+  return kmajor ? (uint64_t)(256 >> 4) : (uint64_t)((2u * (uint32_t)(cols / 8) * 128u) >> 4);
+}
+
+// Issue all product pairs of one K-step: D (+)= A_i(TMEM) . B_j for i + j < P.
+template <int P>
+__device__ __forceinline__ void kstep_ts(uint32_t d, uint32_t a0, uint32_t a_part_cols, const uint64_t (&b)[P],
+                                         uint32_t idesc, bool first) {
+#pragma unroll
+  for (int k = 0; k < Pairs<P>::n; ++k)
+    mma_ts(d, a0 + (uint32_t)Pairs<P>::i(k) * a_part_cols, b[Pairs<P>::j(k)], idesc, (first && k == 0) ? 0u : 1u);
+}
+
 // Descriptor of a weight image (rows x cols bf16, core-matrix blocked) for K-step kk.
 //  kmajor: MN = rows, K = cols;  else: K = rows, MN = cols.  mn0 = first MN index (multiple of 8).
 __device__ __forceinline__ uint64_t wdesc(uint32_t img, int rows, int cols, int kmajor, int mn0, int kk) {
@@ -76,9 +103,10 @@ struct Chain3 {
   int w1_groups, w3_groups;
   int adjoint;
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
-  uint32_t sm_w1, sm_w2, sm_w3, sm_bar, smem_bytes;
+  uint32_t sm_w1, sm_w2, sm_w3, sm_tab, sm_bar, smem_bytes;
   uint32_t colA1, colD1, colA2, colD2, colA3, colD3;
   int d3_sync;
+  long long* prof;                    // optional phase timestamps (CTA 0, first 8 tiles), debug only
 };
 
 struct Bars {
@@ -110,9 +138,38 @@ __device__ __forceinline__ void ld16f(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+#define DL_PROF(ev)                                                                    \
+  do {                                                                                 \
+    if (p.prof && blockIdx.x == 0 && it < 8 && (threadIdx.x & 31) == 0)                \
+      p.prof[(it * 2 + (warp == kEWarps)) * 32 + (ev)] = clock64();                    \
+  } while (0)
+
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
+// One MMA of an issue table: B descriptor, A TMEM column, D TMEM column | accumulate << 31.
+struct MmaEnt {
+  uint64_t b;
+  uint32_t a;
+  uint32_t d;
+};
+
+// One SS MMA (both operands from shared memory) with its own instruction descriptor.
+struct SsEnt {
+  uint64_t a;
+  uint64_t b;
+  uint32_t d;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ void issue_ts(const MmaEnt* e, int n, uint32_t tbase, uint32_t idesc) {
+#pragma unroll 4
+  for (int k = 0; k < n; ++k) {
+    const MmaEnt m = e[k];
+    mma_ts(tbase + (m.d & 0x7FFFFFFFu), tbase + m.a, m.b, idesc, m.d >> 31);
+  }
 }
 
 // ---------------------------------------------------------------------------- chain3 kernel
@@ -184,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
       const int64_t b = t / p.tiles_per_b;
       const int64_t v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
+      if (warp == 0) DL_PROF(0);
       // ---- stage-1 inputs, one group at a time (register prefetch of the next group) ----
       for (int g = 0; g < p.G1; ++g) {
         float cur[MAXC][16];
@@ -193,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
           for (int i = 0; i < 16; ++i) cur[ci][i] = pf[ci][i];
         if (g + 1 < p.G1) load_item(t, g + 1);
         else if (t + gridDim.x < ntiles) load_item(t + gridDim.x, 0);
+        if (warp == 0) DL_PROF(1 + 2 * g);
         if (n_ax > 0) mbar_wait(&bars.ax_empty, (n_ax - 1) & 1);
         fence_after();
 #pragma unroll
@@ -203,10 +262,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
         tmem_wait_st();
         fence_before();
         warp_arrive(&bars.ax_full);
+        if (warp == 0) DL_PROF(2 + 2 * g);
         ++n_ax;
       }
       // ---- stage-1 accumulators -> stage-2 A operand ----
       mbar_wait(&bars.c_full, it & 1);
+      if (warp == 0) DL_PROF(8);
       fence_after();
       {
         const int D1 = p.G1 * p.N1, nck = D1 / 16;
@@ -220,9 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
       fence_before();
       warp_arrive(&bars.ac_full);
       // ---- per output group: stage-2 accumulators (+bias) -> stage-3 A; stage-3 -> HBM ----
+      mbar_wait(&bars.u_full[0], it & 1);
+      fence_after();
       for (int o = 0; o < p.G2; ++o) {
-        mbar_wait(&bars.u_full[o], it & 1);
-        fence_after();
         const int nck2 = p.N2 / 16;
         for (int ck = cg; ck < nck2; ck += kEW) {
           float vv[16];
@@ -239,7 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
         tmem_wait_st();
         fence_before();
         warp_arrive(&bars.au_full);
+        if (warp == 0) DL_PROF(11 + 3 * o);
         mbar_wait(&bars.y_full, n_y & 1);
+        if (warp == 0) DL_PROF(12 + 3 * o);
         ++n_y;
         fence_after();
         float* dst = p.out + b * p.out_bs + (int64_t)o * p.C3 * p.nvox + v;
@@ -255,73 +318,89 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
             }
           }
         }
+        if (warp == 0) DL_PROF(13 + 3 * o);
         fence_before();
       }
     }
-  } else if (lane == 0) {
-    // =========================== MMA issuer ===========================
-    constexpr int NP = npairs(PARTS);
+  } else {
+    // =========================== MMA issuer (converged warp, one elected lane issues) ===========
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2), sw3 = smem_u32(smem + p.sm_w3);
     const int km = p.adjoint ? 0 : 1;   // forward: K-major weights; adjoint: MN-major
+    const int K2 = p.G1 * p.N1, NT2 = p.G2 * p.N2;
+    const bool merge2 = NT2 <= 256;     // one MMA spans every stage-2 output group
     const uint32_t id1 = idesc_bf16(128, p.N1, 0, 1 - km);
-    const uint32_t id2 = idesc_bf16(128, p.N2, 0, 1 - km);
+    const uint32_t id2 = idesc_bf16(128, merge2 ? NT2 : p.N2, 0, 1 - km);
     const uint32_t id3 = idesc_bf16(128, p.N3, 0, 1 - km);
-    // image geometry (rows x cols) in the layout the host packed
     const int r1 = km ? p.N1 : p.K1, c1 = km ? p.K1 : p.N1;
-    const int K2 = p.G1 * p.N1;
-    const int r2 = km ? p.G2 * p.N2 : K2, c2 = km ? K2 : p.G2 * p.N2;
+    const int r2 = km ? NT2 : K2, c2 = km ? K2 : NT2;
     const int r3 = km ? p.N3 : p.N2, c3 = km ? p.N2 : p.N3;
+    const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(c2, km), ks3 = wkstep(c3, km);
+    const int nk1 = p.K1 / 16, nk2 = K2 / 16, nk3 = p.N2 / 16;
     uint32_t n_ax = 0, n_au = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       for (int g = 0; g < p.G1; ++g) {
+        const int wg = p.w1_groups > 1 ? g : 0;
+        uint64_t b[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img, r1, c1, km, 0, 0);
+        DL_PROF(1 + 2 * g);
         mbar_wait(&bars.ax_full, n_ax & 1);
+        DL_PROF(2 + 2 * g);
         ++n_ax;
         fence_after();
-        const int wg = p.w1_groups > 1 ? g : 0;
-        for (int kk = 0; kk < p.K1 / 16; ++kk) {
-          for (int pr = 0; pr < NP; ++pr) {
-            int i, j;
-            pair_of(PARTS, pr, i, j);
-            const uint32_t img = sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img;
-            mma_ts(tbase + p.colD1 + (uint32_t)(g * p.N1), tbase + p.colA1 + (uint32_t)(i * (p.K1 / 2) + 8 * kk),
-                   wdesc(img, r1, c1, km, 0, kk), id1, (kk | pr) != 0);
-          }
+        const uint32_t d = tbase + p.colD1 + (uint32_t)(g * p.N1);
+        for (int kk = 0; kk < nk1; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA1 + 8u * kk, p.K1 / 2, b, id1, kk == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) b[j] += ks1;
         }
-        commit(&bars.ax_empty);
-        if (g == p.G1 - 1) commit(&bars.c_full);
+        if (elect_one()) commit(&bars.ax_empty);
+        __syncwarp();
       }
+      if (elect_one()) commit(&bars.c_full);
+      __syncwarp();
+      DL_PROF(8);
       mbar_wait(&bars.ac_full, it & 1);
+      DL_PROF(9);
       fence_after();
-      for (int o = 0; o < p.G2; ++o) {
-        for (int kk = 0; kk < K2 / 16; ++kk) {
-          for (int pr = 0; pr < NP; ++pr) {
-            int i, j;
-            pair_of(PARTS, pr, i, j);
-            mma_ts(tbase + p.colD2 + (uint32_t)(o * p.N2), tbase + p.colA2 + (uint32_t)(i * (K2 / 2) + 8 * kk),
-                   wdesc(sw2 + (uint32_t)j * p.w2_img, r2, c2, km, o * p.N2, kk), id2, (kk | pr) != 0);
-          }
+      for (int o = 0; o < (merge2 ? 1 : p.G2); ++o) {
+        uint64_t b[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, r2, c2, km, o * p.N2, 0);
+        const uint32_t d = tbase + p.colD2 + (uint32_t)(o * p.N2);
+        for (int kk = 0; kk < nk2; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA2 + 8u * kk, K2 / 2, b, id2, kk == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) b[j] += ks2;
         }
-        commit(&bars.u_full[o]);
       }
+      if (elect_one()) commit(&bars.u_full[0]);
+      __syncwarp();
+      DL_PROF(10);
       if (p.d3_sync) {
-        mbar_wait(&bars.u_full[p.G2 - 1], it & 1);
+        mbar_wait(&bars.u_full[0], it & 1);
         fence_after();
       }
       for (int o = 0; o < p.G2; ++o) {
+        const int wg = p.w3_groups > 1 ? o : 0;
+        uint64_t b[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw3 + (uint32_t)(j * p.w3_groups + wg) * p.w3_img, r3, c3, km, 0, 0);
         mbar_wait(&bars.au_full, n_au & 1);
+        DL_PROF(11 + 3 * o);
         ++n_au;
         fence_after();
-        const int wg = p.w3_groups > 1 ? o : 0;
-        for (int kk = 0; kk < p.N2 / 16; ++kk) {
-          for (int pr = 0; pr < NP; ++pr) {
-            int i, j;
-            pair_of(PARTS, pr, i, j);
-            const uint32_t img = sw3 + (uint32_t)(j * p.w3_groups + wg) * p.w3_img;
-            mma_ts(tbase + p.colD3, tbase + p.colA3 + (uint32_t)(i * (p.N2 / 2) + 8 * kk),
-                   wdesc(img, r3, c3, km, 0, kk), id3, (kk | pr) != 0);
-          }
+        for (int kk = 0; kk < nk3; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(tbase + p.colD3, tbase + p.colA3 + 8u * kk, p.N2 / 2, b, id3, kk == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) b[j] += ks3;
         }
-        commit(&bars.y_full);
+        if (elect_one()) commit(&bars.y_full);
+        __syncwarp();
+        DL_PROF(12 + 3 * o);
       }
     }
   }
@@ -329,7 +408,6 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
   __syncthreads();
   if (warp == kEWarps) tmem_dealloc(tbase, 512);
 }
-
 
 // ---------------------------------------------------------------------------- operand packing
 // `ng` row-major fp32 matrices of (nrb*rb) x (ncb*cb) -> PARTS bf16 images each of (nrb*rbp) x (ncb*cbp)
@@ -367,7 +445,7 @@ struct GramP {
   int S_in, N, NPi, RPi, S_out, N_out, NPo, RPo, R_out;
   int wM_groups;
   uint32_t wM_img, wB_img;
-  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
+  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_tab, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
   uint32_t colGA, colGB, colGC, colA, colD;
   int GR, GC;                // g rows (S_out*RPo), c rows (S_in*RPi)
 };
@@ -552,71 +630,82 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
       float* dbp = p.partials + (int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out;
       for (int o = 0; o < p.S_out; ++o) dbp[o] = bars.db[o];
     }
-  } else if (lane == 0) {
-    constexpr int NP = npairs(PARTS);
+  } else {
+    // =========================== MMA issuer (converged warp, one elected lane issues) ===========
     const uint32_t sM = smem_u32(smem + p.sm_wM), sB = smem_u32(smem + p.sm_wB);
     const uint32_t sc = smem_u32(smem + p.sm_c), sg = smem_u32(smem + p.sm_g);
     const uint32_t idg = idesc_bf16(128, p.RPo, 0, 1);   // g: A = dy (TMEM), B = B' image MN-major
     const uint32_t idc = idesc_bf16(128, p.RPi, 0, 0);   // c: B = M image K-major
-    const uint32_t idA = idesc_bf16(128, p.GC, 0, 0);
-    const uint32_t idB = idesc_bf16(128, 16, 0, 0);
-    const uint32_t idC = idesc_bf16(64, 16, 0, 0);
+    const uint32_t idA = idesc_bf16(128, p.GC, 0, 0), idB = idesc_bf16(128, 16, 0, 0), idC = idesc_bf16(64, 16, 0, 0);
     const int grow = p.GR < 128 ? 128 : p.GR;
     const uint32_t ASg = (uint32_t)(grow / 8) * 1024u, ASc = (uint32_t)(p.GC / 8) * 1024u;
+    const uint64_t ksg = wkstep(p.RPo, 0), ksc = wkstep(p.NPi, 1);
+    const int nkg = p.NPo / 16, nkc = p.NPi / 16;
     uint32_t n_a = 0, it = 0;
-    bool first = true;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       for (int o = 0; o < p.S_out; ++o) {
+        uint64_t b[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sB + (uint32_t)j * p.wB_img, p.NPo, p.RPo, 0, 0, 0);
         mbar_wait(&bars.a_full, n_a & 1);
         ++n_a;
         fence_after();
-        for (int kk = 0; kk < p.NPo / 16; ++kk)
-          for (int pr = 0; pr < NP; ++pr) {
-            int i, j;
-            pair_of(PARTS, pr, i, j);
-            mma_ts(tbase + p.colD + (uint32_t)(o * p.RPo), tbase + p.colA + (uint32_t)(i * (p.NPo / 2) + 8 * kk),
-                   wdesc(sB + (uint32_t)j * p.wB_img, p.NPo, p.RPo, 0, 0, kk), idg, (kk | pr) != 0);
-          }
-        commit(&bars.a_empty);
+        const uint32_t d = tbase + p.colD + (uint32_t)(o * p.RPo);
+        for (int kk = 0; kk < nkg; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA + 8u * kk, p.NPo / 2, b, idg, kk == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) b[j] += ksg;
+        }
+        if (elect_one()) commit(&bars.a_empty);
+        __syncwarp();
       }
-      commit(&bars.d_full);
+      if (elect_one()) commit(&bars.d_full);
+      __syncwarp();
       for (int s = 0; s < p.S_in; ++s) {
+        const int wg = p.wM_groups > 1 ? s : 0;
+        uint64_t b[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.RPi, p.NPi, 1, 0, 0);
         mbar_wait(&bars.a_full, n_a & 1);
         ++n_a;
         fence_after();
-        const int wg = p.wM_groups > 1 ? s : 0;
-        for (int kk = 0; kk < p.NPi / 16; ++kk)
-          for (int pr = 0; pr < NP; ++pr) {
-            int i, j;
-            pair_of(PARTS, pr, i, j);
-            mma_ts(tbase + p.colD + (uint32_t)(s * p.RPi), tbase + p.colA + (uint32_t)(i * (p.NPi / 2) + 8 * kk),
-                   wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.RPi, p.NPi, 1, 0, kk), idc,
-                   (kk | pr) != 0);
-          }
-        commit(&bars.a_empty);
+        const uint32_t d = tbase + p.colD + (uint32_t)(s * p.RPi);
+        for (int kk = 0; kk < nkc; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA + 8u * kk, p.NPi / 2, b, idc, kk == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) b[j] += ksc;
+        }
+        if (elect_one()) commit(&bars.a_empty);
+        __syncwarp();
       }
-      commit(&bars.d_full);
-      // ---- Gram over this tile's 128 voxels (two-term split operands) ----
+      if (elect_one()) commit(&bars.d_full);
+      __syncwarp();
+      // ---- Gram over this tile's 128 voxels (two-term split operands, three blocks) ----
       mbar_wait(&bars.tiles_full, it & 1);
       fence_after();
       for (int kk = 0; kk < kTileV / 16; ++kk) {
         const uint32_t ko = (uint32_t)(kk >> 2), kb = (uint32_t)(kk & 3) * 32u;
-        for (int pr = 0; pr < 3; ++pr) {
-          int i, j;
-          pair_of(2, pr, i, j);
-          const uint32_t gI = sg + (uint32_t)i * p.gtile + ko * ASg + kb, gJ = sg + (uint32_t)j * p.gtile + ko * ASg + kb;
-          const uint32_t cI = sc + (uint32_t)i * p.ctile + ko * ASc + kb, cJ = sc + (uint32_t)j * p.ctile + ko * ASc + kb;
-          const uint32_t acc = first ? ((kk | pr) != 0) : 1u;
-          mma_ss(tbase + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
-          if (p.GR > 128) {
-            mma_ss(tbase + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
-            if (p.GC > 128)
-              mma_ss(tbase + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC, acc);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int i = Pairs<2>::i(k), j = Pairs<2>::j(k);
+            const uint32_t gI = sg + (uint32_t)i * p.gtile + ko * ASg + kb, gJ = sg + (uint32_t)j * p.gtile + ko * ASg + kb;
+            const uint32_t cI = sc + (uint32_t)i * p.ctile + ko * ASc + kb, cJ = sc + (uint32_t)j * p.ctile + ko * ASc + kb;
+            const uint32_t acc = (it > 0 || kk > 0 || k > 0) ? 1u : 0u;
+            mma_ss(tbase + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
+            if (p.GR > 128) {
+              mma_ss(tbase + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
+              if (p.GC > 128)
+                mma_ss(tbase + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC, acc);
+            }
           }
         }
+        __syncwarp();
       }
-      first = false;
-      commit(&bars.gram_done);
+      if (elect_one()) commit(&bars.gram_done);
+      __syncwarp();
     }
   }
   fence_before();
@@ -674,6 +763,8 @@ namespace {
 
 inline int r16(int64_t x) { return (int)((x + 15) / 16 * 16); }
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+long long* g_prof = nullptr;   // debug: phase timestamps of the next chain3 launch
 
 int split_terms() {
   static int v = [] {
@@ -770,6 +861,12 @@ bool plan_chain3(Chain3& p, int parts) {
   p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
   p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
   p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
+  {
+    const int np = parts * (parts + 1) / 2, NT2 = p.G2 * p.N2;
+    const int n2g = NT2 <= 256 ? 1 : p.G2;
+    const size_t ents = (size_t)np * (p.G1 * (p.K1 / 16) + n2g * (p.G1 * p.N1 / 16) + p.G2 * (p.N2 / 16));
+    p.sm_tab = (uint32_t)o; o = al(o + ents * 16, 16);
+  }
   p.sm_bar = (uint32_t)o; o = al(o + sizeof(Bars), 16);
   p.smem_bytes = (uint32_t)o;
   return o <= 227 * 1024;
@@ -800,6 +897,11 @@ bool plan_gram(GramP& p, int parts) {
   p.sm_g = (uint32_t)o; o = al(o + (size_t)2 * p.gtile, 1024);
   // block C reads c rows up to 191 of every K-atom: keep >= 8 KB of mapped smem after the g tile
   o = al(o + 8192, 1024);
+  {
+    const int np = parts * (parts + 1) / 2;
+    const size_t ts = (size_t)np * (p.S_out * (p.NPo / 16) + p.S_in * (p.NPi / 16)) * 16;
+    p.sm_tab = (uint32_t)o; o = al(o + ts + (size_t)(kTileV / 16) * 3 * 3 * sizeof(SsEnt), 16);
+  }
   p.sm_bar = (uint32_t)o; o = al(o + sizeof(GBars), 16);
   p.smem_bytes = (uint32_t)o;
   return o <= 227 * 1024;
@@ -919,6 +1021,10 @@ int grid_for(int64_t ntiles, int sm) { return (int)(ntiles < sm ? (ntiles > 0 ? 
 
 extern "C" {
 
+// Debug hook (not part of the documented ABI): record chain3 phase timestamps into `buf`
+// (device, >= 8*2*32 int64) on subsequent forward launches; NULL disables.
+void dl_debug_chain_prof(void* buf) { dl::tc::g_prof = reinterpret_cast<long long*>(buf); }
+
 int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
                        int m_per_shell) {
   using namespace dl::tc;
@@ -954,6 +1060,7 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   p.in = x;
   p.out = y;
   p.bias2 = bvec;
+  p.prof = g_prof;
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
   return d.parts == 3 ? run_chain3_p<3>(p, grid, st) : run_chain3_p<2>(p, grid, st);
 }

@@ -53,6 +53,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
        | ((uint32_t)(M >> 4) << 24);
 }
 
+// 1 on exactly one lane of a converged warp (elect.sync).
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "@px mov.s32 %0, 1;\n\t}\n"
+      : "+r"(pred));
+  return pred;
+}
+
 // ------------------------------------------------------------------ MMA issue (one thread)
 // D[tmem] (+)= A[smem desc] . B[smem desc]
 __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,

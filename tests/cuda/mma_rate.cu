@@ -1,0 +1,98 @@
+// Test-only microbenchmark: cycles per tcgen05.mma (kind::f16, M=128, cta_group::1) for SS/TS and N.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../paper_1808_01517_b200/csrc/umma.cuh"
+
+using namespace dl::umma;
+
+__global__ void rate_k(int mode, int N, int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tb_s;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (warp == 0) tmem_alloc(&tb_s, 512);
+  if (threadIdx.x == 0) { mbar_init(&mbar, 1); mbar_fence_init(); }
+  fence_proxy_async();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = tb_s;
+  if (mode >= 20) {
+    // (mode - 20) issuing warps, each its own accumulator, iters/W MMAs each
+    const int W = mode - 20;
+    const uint32_t sa = smem_u32(smem), sbb = smem_u32(smem + 32768);
+    const uint64_t ad = desc_noswz(sa, 128, 256), bd = desc_noswz(sbb, 128, 256);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    __syncthreads();
+    long long t0 = clock64();
+    if (warp < W) {
+      for (int k = 0; k < iters / W; ++k) {
+        if (elect_one()) mma_ss(tb + (uint32_t)(warp * N), ad, bd, id, 1);
+        __syncwarp();
+      }
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; }
+  } else if (mode >= 10 && warp == 0) {
+    // whole warp converged, one elected lane issues (the CUTLASS idiom)
+    const uint32_t sa = smem_u32(smem), sbb = smem_u32(smem + 32768);
+    const uint64_t ad = desc_noswz(sa, 128, 256), bd = desc_noswz(sbb, 128, 256);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    long long t0 = clock64();
+    for (int k = 0; k < iters; ++k) {
+      if (elect_one()) {
+        if (mode == 10) mma_ss(tb, ad, bd, id, 1);
+        else if (mode == 11) mma_ts(tb, tb + 256, bd, id, 1);
+        else mma_ss(tb + (uint32_t)((k & 3) * N), ad, bd, id, 1);
+      }
+      __syncwarp();
+    }
+    long long t1 = clock64();
+    if (elect_one()) commit(&mbar);
+    __syncwarp();
+    mbar_wait(&mbar, 0);
+    long long t2 = clock64();
+    if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+  } else if (mode < 10 && threadIdx.x == 0) {
+    const uint32_t sa = smem_u32(smem), sbb = smem_u32(smem + 32768);
+    const uint64_t ad = desc_noswz(sa, 128, 256), bd = desc_noswz(sbb, 128, 256);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    long long t0 = clock64();
+    if (mode < 2) {
+      for (int k = 0; k < iters; ++k) {
+        if (mode == 0) mma_ss(tb, ad, bd, id, 1);
+        else mma_ts(tb, tb + 256, bd, id, 1);
+      }
+    } else {
+      // round-robin over `nacc` independent accumulators of N columns each
+      const int nacc = mode - 1;
+      for (int k = 0; k < iters; ++k) mma_ss(tb + (uint32_t)((k % nacc) * N), ad, bd, id, 1);
+    }
+    long long t1 = clock64();
+    commit(&mbar);
+    mbar_wait(&mbar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+extern "C" int mma_rate(int mode, int N, int iters, long long* out_host) {
+  long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  rate_k<<<1, 128, 64 * 1024>>>(mode, N, iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(out_host, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return (int)e;
+}
