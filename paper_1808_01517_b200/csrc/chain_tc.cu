@@ -4,21 +4,24 @@
 // lsc.lsc_forward (lsc.py:158-199, folded as c_out = L c + bias*beta) ->
 // fitting.sh_to_signal (fitting.py:239-250); the backward is the adjoint (SPEC.md:12 leaves it out).
 //
-// Design (one persistent CTA per SM, voxel tiles of 128 = the MMA M dimension):
-//  * thread t of a TMEM lane quadrant owns voxel t of the tile: it loads its voxel's channels
-//    with coalesced 4-byte loads (a warp covers 32 consecutive voxels of one channel row),
-//    splits every fp32 value into PARTS bf16 terms and writes them into TMEM as the A operand;
-//  * all weights (M, folded LSC operator L, B') are staged ONCE per CTA in shared memory as
-//    PARTS bf16 terms (core-matrix blocked images; the same image serves the forward (K-major)
-//    and the adjoint (MN-major) product);
-//  * one elected thread issues tcgen05.mma kind::f16 (A from TMEM, B from smem, fp32 accumulate in
-//    TMEM) for every product pair (a_i, w_j) with i + j < PARTS, i.e. an fp32-accurate split product;
-//  * the accumulators of a stage are read back (tcgen05.ld), split again and written as the next
-//    stage's A operand -- the intermediates c and u never touch HBM.
-// chain3_tc runs stage1 (per input group) -> stage2 (dense across groups) -> stage3 (per output
-// group): forward x -> y (W1 = M, W2 = L, W3 = B', + bias) and adjoint dy -> dx (W1 = B', W2 = L,
-// W3 = M; transposed descriptors).  gram_tc computes the LSC weight Gram G = sum_v g c^T with
-// g = B'^T dy and c = M x produced on the tensor cores and staged in SWIZZLE_128B smem tiles.
+// One persistent CTA per SM walks voxel tiles of 128 (= the MMA M dimension), warp-specialised:
+//   warp 13      TMA loader: 1-D bulk copies (cp.async.bulk) of 16-channel x 128-voxel row blocks
+//                into a shared-memory ring (rows are copied from the 16-byte aligned address below
+//                the tile start, so any voxel count works; the shift is stored beside the rows);
+//   warps 0-3    IN: thread t owns voxel t; reads its 16 values, splits each fp32 into PARTS bf16
+//                terms and writes them into a TMEM A-operand slot (lane = voxel);
+//   warp 12      MMA: one elected lane issues tcgen05.mma kind::f16 (A from TMEM, B = weights
+//                from shared memory, fp32 accumulate in TMEM) for every term pair i + j < PARTS;
+//   warps 4-11   MID: accumulator -> next stage's A operand (split again), the LSC bias, and the
+//                final tcgen05.ld -> coalesced global stores.
+// chain3: stage1 (per input group) -> stage2 (all groups, one N <= 256 MMA) -> stage3 (per output
+// group).  Forward x -> y uses W1 = M, W2 = L, W3 = B' (+ bias); the adjoint dy -> dx uses the same
+// shared-memory images through transposed (MN-major) descriptors.  With enough TMEM the next
+// tile's stage 1 is interleaved with this tile's stage 3.
+// gram: g = B'^T dy and c = M x on the tensor cores, staged as two-term bf16 SWIZZLE_128B tiles,
+// G = sum_v g c^T accumulated in TMEM for the whole CTA, then a float64 finalize dW = <P_k, G>.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "umma.cuh"
@@ -28,31 +31,20 @@ namespace tc {
 
 using namespace dl::umma;
 
-constexpr int kTileV = 128;          // voxels per tile (MMA M)
-constexpr int kEW = 2;               // epilogue warps per TMEM lane quadrant
-constexpr int kEWarps = 4 * kEW;     // 8 epilogue warps
-constexpr int kThreads = (kEWarps + 1) * 32;
+constexpr int kTileV = 128;                 // voxels per tile (MMA M)
+constexpr int kIN = 4;                      // input-conversion warps (one per TMEM lane quadrant)
+constexpr int kMID = 8;                     // epilogue warps (two per quadrant)
+constexpr int kWarpMMA = kIN + kMID;        // 12
+constexpr int kWarpLD = kWarpMMA + 1;       // 13
+constexpr int kThreads = (kWarpLD + 1) * 32;
+constexpr int kRowBytes = 528;              // 128 voxels + <= 3 floats of alignment shift, 16-B multiple
+constexpr int kChunkBytes = 16 * kRowBytes + 64;   // 16 rows + their 16 shifts
+constexpr int kMaxStages = 8;
+constexpr int kMaxSlots = 6;
 
-__host__ __device__ constexpr int npairs(int parts) { return parts * (parts + 1) / 2; }
-
-// (i, j) product pairs of a `parts`-term split with i + j < parts, small terms first.
-__device__ __forceinline__ void pair_of(int parts, int idx, int& i, int& j) {
-  if (parts == 3) {
-    const int pi[6] = {2, 1, 0, 1, 0, 0}, pj[6] = {0, 1, 2, 0, 1, 0};
-    i = pi[idx];
-    j = pj[idx];
-  } else if (parts == 2) {
-    const int pi[3] = {1, 0, 0}, pj[3] = {0, 1, 0};
-    i = pi[idx];
-    j = pj[idx];
-  } else {
-    i = j = 0;
-  }
-}
-
-// Compile-time (i, j) pair lists (activation term i, weight term j).
+// ---------------------------------------------------------------------------- small helpers
 template <int P> struct Pairs;
-template <> struct Pairs<3> {
+template <> struct Pairs<3> {   // (i, j): activation term i x weight term j, i + j < 3, small first
   static constexpr int n = 6;
   __device__ static constexpr int i(int k) { return k == 0 ? 2 : k == 1 ? 1 : k == 2 ? 0 : k == 3 ? 1 : 0; }
   __device__ static constexpr int j(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? 0 : k == 4 ? 1 : 0; }
@@ -63,68 +55,40 @@ template <> struct Pairs<2> {
   __device__ static constexpr int j(int k) { return k == 1 ? 1 : 0; }
 };
 
-// Byte advance of a weight descriptor per K-step (added to the start-address field, >> 4).
+// Weight-image descriptor (rows x cols bf16, core-matrix blocked, umma.cuh) at K-step 0.
+//  kmajor: MN = rows, K = cols;  else: K = rows, MN = cols.  mn0: first MN index (multiple of 8).
+__device__ __forceinline__ uint64_t wdesc(uint32_t img, int cols, int kmajor, int mn0) {
+  if (kmajor) {
+    const uint32_t sbo = (uint32_t)(cols / 8) * 128u;
+    return desc_noswz(img + (uint32_t)(mn0 / 8) * sbo, 128u, sbo);
+  }
+  const uint32_t lbo = (uint32_t)(cols / 8) * 128u;
+  return desc_noswz(img + (uint32_t)(mn0 / 8) * 128u, lbo, 128u);
+}
+// Descriptor advance per K-step of 16 (start-address field, 16-byte units).
 __device__ __forceinline__ uint64_t wkstep(int cols, int kmajor) {
   return kmajor ? (uint64_t)(256 >> 4) : (uint64_t)((2u * (uint32_t)(cols / 8) * 128u) >> 4);
 }
 
-// Issue all product pairs of one K-step: D (+)= A_i(TMEM) . B_j for i + j < P.
+// All term pairs of one K-step: D (+)= A_i (TMEM, part stride a_part cols) . B_j.
 template <int P>
-__device__ __forceinline__ void kstep_ts(uint32_t d, uint32_t a0, uint32_t a_part_cols, const uint64_t (&b)[P],
+__device__ __forceinline__ void kstep_ts(uint32_t d, uint32_t a0, uint32_t a_part, const uint64_t (&b)[P],
                                          uint32_t idesc, bool first) {
 #pragma unroll
   for (int k = 0; k < Pairs<P>::n; ++k)
-    mma_ts(d, a0 + (uint32_t)Pairs<P>::i(k) * a_part_cols, b[Pairs<P>::j(k)], idesc, (first && k == 0) ? 0u : 1u);
+    mma_ts(d, a0 + (uint32_t)Pairs<P>::i(k) * a_part, b[Pairs<P>::j(k)], idesc, (first && k == 0) ? 0u : 1u);
 }
 
-// Descriptor of a weight image (rows x cols bf16, core-matrix blocked) for K-step kk.
-//  kmajor: MN = rows, K = cols;  else: K = rows, MN = cols.  mn0 = first MN index (multiple of 8).
-__device__ __forceinline__ uint64_t wdesc(uint32_t img, int rows, int cols, int kmajor, int mn0, int kk) {
-  if (kmajor) {
-    const uint32_t sbo = (uint32_t)(cols / 8) * 128u;
-    return desc_noswz(img + (uint32_t)(mn0 / 8) * sbo + (uint32_t)kk * 256u, 128u, sbo);
-  }
-  const uint32_t lbo = (uint32_t)(cols / 8) * 128u;
-  return desc_noswz(img + (uint32_t)(mn0 / 8) * 128u + (uint32_t)kk * 2u * lbo, lbo, 128u);
-  (void)rows;
-}
-
-struct Chain3 {
-  const float* in;
-  float* out;
-  const float* bias2;                 // real stage-2 bias per (group, channel < C2) or null
-  const uint16_t* w1;                 // images, part-major: (q * groups + g) * img_bytes
-  const uint16_t* w2;
-  const uint16_t* w3;
-  int64_t nbatch, nvox, in_bs, out_bs, tiles_per_b;
-  int G1, C1, K1, N1;                 // stage 1: groups, real in-ch/group, padded K, padded N
-  int G2, C2, N2;                     // stage 2: groups, real out-ch/group, padded N
-  int C3, N3;                         // stage 3: real / padded out-ch per group
-  int w1_groups, w3_groups;
-  int adjoint;
-  uint32_t w1_img, w2_img, w3_img;    // bytes per image
-  uint32_t sm_w1, sm_w2, sm_w3, sm_tab, sm_bar, smem_bytes;
-  uint32_t colA1, colD1, colA2, colD2, colA3, colD3;
-  int d3_sync;
-  long long* prof;                    // optional phase timestamps (CTA 0, first 8 tiles), debug only
-};
-
-struct Bars {
-  uint64_t ax_full, ax_empty, c_full, ac_full, au_full, y_full;
-  uint64_t u_full[4];
-  uint32_t tmem_base;
-};
-
-// ---------------------------------------------------------------------------- epilogue helpers
+// 16 fp32 values of one voxel -> PARTS bf16 terms -> TMEM (8 packed columns per term).
 template <int PARTS>
 __device__ __forceinline__ void split_store16(uint32_t taddr_part0, uint32_t part_stride_cols, const float (&v)[16]) {
   uint32_t w[PARTS][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    uint32_t p[PARTS];
-    split_pair<PARTS>(v[2 * i], v[2 * i + 1], p);
+    uint32_t pp[PARTS];
+    split_pair<PARTS>(v[2 * i], v[2 * i + 1], pp);
 #pragma unroll
-    for (int q = 0; q < PARTS; ++q) w[q][i] = p[q];
+    for (int q = 0; q < PARTS; ++q) w[q][i] = pp[q];
   }
 #pragma unroll
   for (int q = 0; q < PARTS; ++q) tmem_st<8>(taddr_part0 + (uint32_t)q * part_stride_cols, w[q]);
@@ -138,71 +102,138 @@ __device__ __forceinline__ void ld16f(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-#define DL_PROF(ev)                                                                    \
-  do {                                                                                 \
-    if (p.prof && blockIdx.x == 0 && it < 8 && (threadIdx.x & 31) == 0)                \
-      p.prof[(it * 2 + (warp == kEWarps)) * 32 + (ev)] = clock64();                    \
-  } while (0)
-
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
-// One MMA of an issue table: B descriptor, A TMEM column, D TMEM column | accumulate << 31.
-struct MmaEnt {
-  uint64_t b;
-  uint32_t a;
-  uint32_t d;
-};
+// byte offset of (row j, voxel k) in a SWIZZLE_128B K-major tile with `rows` rows (K = 128 voxels)
+__device__ __forceinline__ uint32_t sw128_off(int j, int k, int rows) {
+  return (uint32_t)(k >> 6) * (uint32_t)(rows >> 3) * 1024u + (uint32_t)(j >> 3) * 1024u + (uint32_t)(j & 7) * 128u +
+         (uint32_t)((((k & 63) >> 3) ^ (j & 7)) << 4) + (uint32_t)(k & 7) * 2u;
+}
 
-// One SS MMA (both operands from shared memory) with its own instruction descriptor.
-struct SsEnt {
-  uint64_t a;
-  uint64_t b;
-  uint32_t d;
-  uint32_t idesc;
-};
+// A tile is "safe" for the bulk loader when every copied row (<= 132 floats from the aligned
+// address below the tile start) stays inside the tensor.
+__device__ __forceinline__ bool tile_safe(int64_t b, int64_t v0, int64_t nvox, int base_aligned) {
+  return v0 + kTileV + 4 <= nvox && (v0 >= 4 || b > 0 || base_aligned);
+}
 
-__device__ __forceinline__ void issue_ts(const MmaEnt* e, int n, uint32_t tbase, uint32_t idesc) {
-#pragma unroll 4
-  for (int k = 0; k < n; ++k) {
-    const MmaEnt m = e[k];
-    mma_ts(tbase + (m.d & 0x7FFFFFFFu), tbase + m.a, m.b, idesc, m.d >> 31);
+// ---------------------------------------------------------------------------- loader (one warp)
+// Bulk copies of the 16-row chunk `k` of one channel group (C real channels, src already offset
+// to the tile's first voxel) into a ring stage; unsafe tiles only arrive (IN loads directly).
+__device__ __forceinline__ void load_chunk(uint8_t* stage_ptr, uint64_t* full, const float* src_g, int C, int k,
+                                           int64_t nvox, bool safe) {
+  const int lane = threadIdx.x & 31;
+  if (!safe) {
+    if (lane == 0) mbar_arrive(full);
+    __syncwarp();
+    return;
+  }
+  const int c = 16 * k + lane;
+  const bool valid = lane < 16 && c < C;
+  uint32_t bytes = 0, shift = 0;
+  const float* a = nullptr;
+  if (valid) {
+    const float* row = src_g + (int64_t)c * nvox;
+    shift = (uint32_t)((reinterpret_cast<uintptr_t>(row) >> 2) & 3u);
+    a = row - shift;
+    bytes = ((128u + shift) * 4u + 15u) & ~15u;
+  }
+  if (lane < 16) reinterpret_cast<uint32_t*>(stage_ptr + 16 * kRowBytes)[lane] = shift;
+  uint32_t total = bytes;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
+  __syncwarp();
+  if (lane == 0) mbar_arrive_tx(full, total);
+  __syncwarp();
+  if (valid) bulk_g2s(stage_ptr + lane * kRowBytes, a, bytes, full);
+  __syncwarp();
+}
+
+// 16 channel values of this thread's voxel from a staged chunk (or directly from HBM for unsafe tiles)
+__device__ __forceinline__ void read_chunk(const uint8_t* stage_ptr, const float* src_g, int C, int k, int64_t nvox,
+                                           int64_t v0, int row, bool safe, float (&v)[16]) {
+  if (safe) {
+    const uint32_t* sh = reinterpret_cast<const uint32_t*>(stage_ptr + 16 * kRowBytes);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      v[r] = (16 * k + r < C) ? reinterpret_cast<const float*>(stage_ptr + r * kRowBytes)[sh[r] + row] : 0.f;
+  } else {
+    const bool ok = v0 + row < nvox;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int c = 16 * k + r;
+      v[r] = (c < C && ok) ? __ldg(src_g + (int64_t)c * nvox + row) : 0.f;
+    }
   }
 }
 
-// ---------------------------------------------------------------------------- chain3 kernel
-template <int PARTS, int MAXC>
+// ============================================================================ chain3 kernel
+struct Chain3 {
+  const float* in;
+  float* out;
+  const float* bias2;                 // real stage-2 bias per (group, channel < C2) or null
+  const uint16_t* w1;                 // images, part-major: (q * groups + g) * img_bytes
+  const uint16_t* w2;
+  const uint16_t* w3;
+  int64_t nbatch, nvox, in_bs, out_bs, tiles_per_b;
+  int G1, C1, K1, N1;                 // stage 1: groups, real in-ch/group, padded K, padded N
+  int G2, C2, N2;                     // stage 2: groups, real out-ch/group, padded N
+  int C3, N3;                         // stage 3: real / padded out-ch per group
+  int w1_groups, w3_groups;
+  int adjoint, overlap, free_at, base_aligned;
+  int NS, NA;                         // loader ring stages, TMEM A slots
+  uint32_t w1_img, w2_img, w3_img;    // bytes per image
+  uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
+  uint32_t colA, colD1, colA2, colD2, colA3, colD3;
+};
+
+struct Bars3 {
+  uint64_t ld_full[kMaxStages], ld_empty[kMaxStages], a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t d1_full, d1_free, ac_full, u_full, au_full, y_full;
+  uint32_t tmem_base;
+};
+
+template <int PARTS>
 __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  Bars& bars = *reinterpret_cast<Bars*>(smem + p.sm_bar);
+  Bars3& bars = *reinterpret_cast<Bars3*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kSlotW = PARTS * 8;
 
-  // ---- stage all weight images once per CTA ----
-  {
-    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img;
-    const uint32_t b2 = (uint32_t)PARTS * p.w2_img;
-    const uint32_t b3 = (uint32_t)PARTS * p.w3_groups * p.w3_img;
-    const uint4* s1 = reinterpret_cast<const uint4*>(p.w1);
-    const uint4* s2 = reinterpret_cast<const uint4*>(p.w2);
-    const uint4* s3 = reinterpret_cast<const uint4*>(p.w3);
-    uint4* d1 = reinterpret_cast<uint4*>(smem + p.sm_w1);
-    uint4* d2 = reinterpret_cast<uint4*>(smem + p.sm_w2);
-    uint4* d3 = reinterpret_cast<uint4*>(smem + p.sm_w3);
+  {  // stage weight images + bias once per CTA
+    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = (uint32_t)PARTS * p.w2_img,
+                   b3 = (uint32_t)PARTS * p.w3_groups * p.w3_img;
+    const uint4 *s1 = reinterpret_cast<const uint4*>(p.w1), *s2 = reinterpret_cast<const uint4*>(p.w2),
+                *s3 = reinterpret_cast<const uint4*>(p.w3);
+    uint4 *d1 = reinterpret_cast<uint4*>(smem + p.sm_w1), *d2 = reinterpret_cast<uint4*>(smem + p.sm_w2),
+          *d3 = reinterpret_cast<uint4*>(smem + p.sm_w3);
     for (uint32_t i = threadIdx.x; i < b1 / 16; i += blockDim.x) d1[i] = __ldg(s1 + i);
     for (uint32_t i = threadIdx.x; i < b2 / 16; i += blockDim.x) d2[i] = __ldg(s2 + i);
     for (uint32_t i = threadIdx.x; i < b3 / 16; i += blockDim.x) d3[i] = __ldg(s3 + i);
+    float* sb = reinterpret_cast<float*>(smem + p.sm_bias);
+    for (int i = threadIdx.x; i < p.G2 * p.N2; i += blockDim.x) {
+      const int o = i / p.N2, r = i - o * p.N2;
+      sb[i] = (p.bias2 && r < p.C2) ? __ldg(p.bias2 + o * p.C2 + r) : 0.f;
+    }
   }
-  if (warp == kEWarps) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpLD) tmem_alloc(&bars.tmem_base, 512);
   if (threadIdx.x == 0) {
-    mbar_init(&bars.ax_full, kEWarps);
-    mbar_init(&bars.ax_empty, 1);
-    mbar_init(&bars.c_full, 1);
-    mbar_init(&bars.ac_full, kEWarps);
-    mbar_init(&bars.au_full, kEWarps);
+    for (int s = 0; s < p.NS; ++s) {
+      mbar_init(&bars.ld_full[s], 1);
+      mbar_init(&bars.ld_empty[s], kIN);
+    }
+    for (int s = 0; s < p.NA; ++s) {
+      mbar_init(&bars.a_full[s], kIN);
+      mbar_init(&bars.a_empty[s], 1);
+    }
+    mbar_init(&bars.d1_full, 1);
+    mbar_init(&bars.d1_free, kMID);
+    mbar_init(&bars.ac_full, kMID);
+    mbar_init(&bars.u_full, 1);
+    mbar_init(&bars.au_full, kMID);
     mbar_init(&bars.y_full, 1);
-    for (int o = 0; o < 4; ++o) mbar_init(&bars.u_full[o], 1);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -211,229 +242,202 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
   fence_after();
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
+  const int nk1 = p.K1 / 16;
+  uint8_t* ring = smem + p.sm_ring;
 
-  if (warp < kEWarps) {
-    // =========================== epilogue / loader warps ===========================
-    const int qd = warp & 3, cg = warp >> 2;
+  if (warp == kWarpLD) {
+    // =========================== TMA loader ===========================
+    uint32_t seq = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
+      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
+      for (int g = 0; g < p.G1; ++g) {
+        const float* src = p.in + b * p.in_bs + (int64_t)g * p.C1 * p.nvox + v0;
+        for (int k = 0; k < nk1; ++k, ++seq) {
+          const uint32_t s = seq % p.NS;
+          if (seq >= (uint32_t)p.NS) mbar_wait(&bars.ld_empty[s], ((seq / p.NS) - 1) & 1);
+          load_chunk(ring + s * kChunkBytes, &bars.ld_full[s], src, p.C1, k, p.nvox, safe);
+        }
+      }
+    }
+  } else if (warp < kIN) {
+    // =========================== IN: staged rows -> split -> TMEM A slots ===========================
+    const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
+    const int row = 32 * warp + lane;
+    uint32_t seq = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
+      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
+      for (int g = 0; g < p.G1; ++g) {
+        const float* src = p.in + b * p.in_bs + (int64_t)g * p.C1 * p.nvox + v0;
+        for (int k = 0; k < nk1; ++k, ++seq) {
+          const uint32_t s = seq % p.NS, a = seq % p.NA;
+          mbar_wait(&bars.ld_full[s], (seq / p.NS) & 1);
+          float v[16];
+          read_chunk(ring + s * kChunkBytes, src, p.C1, k, p.nvox, v0, row, safe, v);
+          warp_arrive(&bars.ld_empty[s]);
+          if (seq >= (uint32_t)p.NA) mbar_wait(&bars.a_empty[a], ((seq / p.NA) - 1) & 1);
+          fence_after();
+          split_store16<PARTS>(tq + p.colA + a * kSlotW, 8, v);
+          tmem_wait_st();
+          fence_before();
+          warp_arrive(&bars.a_full[a]);
+        }
+      }
+    }
+  } else if (warp < kWarpMMA) {
+    // =========================== MID: accumulators -> next A / HBM ===========================
+    const int mw = warp - kIN, qd = mw & 3, cg = mw >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
     const int row = 32 * qd + lane;
-    const int nck1 = p.K1 / 16;
-    float pf[MAXC][16];
-    auto load_item = [&](int64_t t, int g) {
-      const int64_t b = t / p.tiles_per_b;
-      const int64_t v = (t - b * p.tiles_per_b) * kTileV + row;
-      const bool ok = v < p.nvox;
-      const float* src = p.in + b * p.in_bs + (int64_t)g * p.C1 * p.nvox + v;
-#pragma unroll
-      for (int ci = 0; ci < MAXC; ++ci) {
-        const int ck = cg + ci * kEW;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = ck * 16 + i;
-          pf[ci][i] = (ck < nck1 && n < p.C1 && ok) ? __ldg(src + (int64_t)n * p.nvox) : 0.f;
-        }
-      }
-    };
-    uint32_t n_ax = 0, n_y = 0, it = 0;
-    int64_t t = blockIdx.x;
-    if (t < ntiles) load_item(t, 0);
-    for (; t < ntiles; t += gridDim.x, ++it) {
-      const int64_t b = t / p.tiles_per_b;
-      const int64_t v = (t - b * p.tiles_per_b) * kTileV + row;
+    const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
+    const int D1w = p.G1 * p.N1;
+    uint32_t it = 0, n_y = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
-      if (warp == 0) DL_PROF(0);
-      // ---- stage-1 inputs, one group at a time (register prefetch of the next group) ----
-      for (int g = 0; g < p.G1; ++g) {
-        float cur[MAXC][16];
-#pragma unroll
-        for (int ci = 0; ci < MAXC; ++ci)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) cur[ci][i] = pf[ci][i];
-        if (g + 1 < p.G1) load_item(t, g + 1);
-        else if (t + gridDim.x < ntiles) load_item(t + gridDim.x, 0);
-        if (warp == 0) DL_PROF(1 + 2 * g);
-        if (n_ax > 0) mbar_wait(&bars.ax_empty, (n_ax - 1) & 1);
-        fence_after();
-#pragma unroll
-        for (int ci = 0; ci < MAXC; ++ci) {
-          const int ck = cg + ci * kEW;
-          if (ck < nck1) split_store16<PARTS>(tq + p.colA1 + (uint32_t)ck * 8, p.K1 / 2, cur[ci]);
-        }
-        tmem_wait_st();
-        fence_before();
-        warp_arrive(&bars.ax_full);
-        if (warp == 0) DL_PROF(2 + 2 * g);
-        ++n_ax;
-      }
-      // ---- stage-1 accumulators -> stage-2 A operand ----
-      mbar_wait(&bars.c_full, it & 1);
-      if (warp == 0) DL_PROF(8);
+      mbar_wait(&bars.d1_full, it & 1);
       fence_after();
-      {
-        const int D1 = p.G1 * p.N1, nck = D1 / 16;
-        for (int ck = cg; ck < nck; ck += kEW) {
-          float vv[16];
-          ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
-          split_store16<PARTS>(tq + p.colA2 + (uint32_t)ck * 8, D1 / 2, vv);
-        }
+      for (int ck = cg; ck < D1w / 16; ck += 2) {
+        float vv[16];
+        ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
+        split_store16<PARTS>(tq + p.colA2 + (uint32_t)ck * 8, D1w / 2, vv);
       }
       tmem_wait_st();
       fence_before();
       warp_arrive(&bars.ac_full);
-      // ---- per output group: stage-2 accumulators (+bias) -> stage-3 A; stage-3 -> HBM ----
-      mbar_wait(&bars.u_full[0], it & 1);
+      if (p.free_at == 0) warp_arrive(&bars.d1_free);
+      mbar_wait(&bars.u_full, it & 1);
       fence_after();
       for (int o = 0; o < p.G2; ++o) {
-        const int nck2 = p.N2 / 16;
-        for (int ck = cg; ck < nck2; ck += kEW) {
+        for (int ck = cg; ck < p.N2 / 16; ck += 2) {
           float vv[16];
           ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + ck * 16), vv);
-          if (p.bias2) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int r = ck * 16 + i;
-              if (r < p.C2) vv[i] += __ldg(p.bias2 + o * p.C2 + r);
-            }
-          }
+          for (int i = 0; i < 16; ++i) vv[i] += sb[o * p.N2 + ck * 16 + i];
           split_store16<PARTS>(tq + p.colA3 + (uint32_t)ck * 8, p.N2 / 2, vv);
         }
         tmem_wait_st();
         fence_before();
         warp_arrive(&bars.au_full);
-        if (warp == 0) DL_PROF(11 + 3 * o);
+        if (p.free_at == 1 && o == p.G2 - 1) warp_arrive(&bars.d1_free);   // D2 (aliasing D1) fully read
         mbar_wait(&bars.y_full, n_y & 1);
-        if (warp == 0) DL_PROF(12 + 3 * o);
         ++n_y;
         fence_after();
         float* dst = p.out + b * p.out_bs + (int64_t)o * p.C3 * p.nvox + v;
-        const int nck3 = p.N3 / 16;
-        for (int ck = cg; ck < nck3; ck += kEW) {
+        for (int ck = cg; ck < p.N3 / 16; ck += 2) {
           float vv[16];
           ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
           if (vok) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = ck * 16 + i;
-              if (n < p.C3) __stcs(dst + (int64_t)n * p.nvox, vv[i]);
-            }
+            for (int i = 0; i < 16; ++i)
+              if (ck * 16 + i < p.C3) __stcs(dst + (int64_t)(ck * 16 + i) * p.nvox, vv[i]);
           }
         }
-        if (warp == 0) DL_PROF(13 + 3 * o);
         fence_before();
       }
+      if (p.free_at == 2) warp_arrive(&bars.d1_free);   // stage-3 buffers (in D1) fully read
     }
   } else {
     // =========================== MMA issuer (converged warp, one elected lane issues) ===========
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2), sw3 = smem_u32(smem + p.sm_w3);
     const int km = p.adjoint ? 0 : 1;   // forward: K-major weights; adjoint: MN-major
     const int K2 = p.G1 * p.N1, NT2 = p.G2 * p.N2;
-    const bool merge2 = NT2 <= 256;     // one MMA spans every stage-2 output group
+    const bool merge2 = NT2 <= 256;
     const uint32_t id1 = idesc_bf16(128, p.N1, 0, 1 - km);
     const uint32_t id2 = idesc_bf16(128, merge2 ? NT2 : p.N2, 0, 1 - km);
     const uint32_t id3 = idesc_bf16(128, p.N3, 0, 1 - km);
-    const int r1 = km ? p.N1 : p.K1, c1 = km ? p.K1 : p.N1;
-    const int r2 = km ? NT2 : K2, c2 = km ? K2 : NT2;
-    const int r3 = km ? p.N3 : p.N2, c3 = km ? p.N2 : p.N3;
+    const int c1 = km ? p.K1 : p.N1, c2 = km ? K2 : NT2, c3 = km ? p.N2 : p.N3;
     const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(c2, km), ks3 = wkstep(c3, km);
-    const int nk1 = p.K1 / 16, nk2 = K2 / 16, nk3 = p.N2 / 16;
-    uint32_t n_ax = 0, n_au = 0, it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      for (int g = 0; g < p.G1; ++g) {
-        const int wg = p.w1_groups > 1 ? g : 0;
-        uint64_t b[PARTS];
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img, r1, c1, km, 0, 0);
-        DL_PROF(1 + 2 * g);
-        mbar_wait(&bars.ax_full, n_ax & 1);
-        DL_PROF(2 + 2 * g);
-        ++n_ax;
+    uint32_t seq = 0, n_au = 0;
+    auto s1g = [&](uint32_t it, int g) {
+      if (g == 0 && it > 0) {
+        mbar_wait(&bars.d1_free, (it - 1) & 1);
         fence_after();
-        const uint32_t d = tbase + p.colD1 + (uint32_t)(g * p.N1);
-        for (int kk = 0; kk < nk1; ++kk) {
-          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA1 + 8u * kk, p.K1 / 2, b, id1, kk == 0);
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) b[j] += ks1;
-        }
-        if (elect_one()) commit(&bars.ax_empty);
-        __syncwarp();
       }
-      if (elect_one()) commit(&bars.c_full);
-      __syncwarp();
-      DL_PROF(8);
+      const int wg = p.w1_groups > 1 ? g : 0;
+      uint64_t bd[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) bd[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img, c1, km, 0);
+      const uint32_t d = tbase + p.colD1 + (uint32_t)(g * p.N1);
+      for (int k = 0; k < nk1; ++k, ++seq) {
+        const uint32_t a = seq % p.NA;
+        mbar_wait(&bars.a_full[a], (seq / p.NA) & 1);
+        fence_after();
+        if (elect_one()) {
+          kstep_ts<PARTS>(d, tbase + p.colA + a * kSlotW, 8, bd, id1, k == 0);
+          commit(&bars.a_empty[a]);
+          if (k == nk1 - 1 && g == p.G1 - 1) commit(&bars.d1_full);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd[j] += ks1;
+      }
+    };
+    auto s2 = [&](uint32_t it) {
       mbar_wait(&bars.ac_full, it & 1);
-      DL_PROF(9);
       fence_after();
       for (int o = 0; o < (merge2 ? 1 : p.G2); ++o) {
-        uint64_t b[PARTS];
+        uint64_t bd[PARTS];
 #pragma unroll
-        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, r2, c2, km, o * p.N2, 0);
+        for (int j = 0; j < PARTS; ++j) bd[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, c2, km, o * p.N2);
         const uint32_t d = tbase + p.colD2 + (uint32_t)(o * p.N2);
-        for (int kk = 0; kk < nk2; ++kk) {
-          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA2 + 8u * kk, K2 / 2, b, id2, kk == 0);
+        for (int kk = 0; kk < K2 / 16; ++kk) {
+          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA2 + 8u * kk, K2 / 2, bd, id2, kk == 0);
           __syncwarp();
 #pragma unroll
-          for (int j = 0; j < PARTS; ++j) b[j] += ks2;
+          for (int j = 0; j < PARTS; ++j) bd[j] += ks2;
         }
       }
-      if (elect_one()) commit(&bars.u_full[0]);
+      if (elect_one()) commit(&bars.u_full);
       __syncwarp();
-      DL_PROF(10);
-      if (p.d3_sync) {
-        mbar_wait(&bars.u_full[0], it & 1);
-        fence_after();
-      }
-      for (int o = 0; o < p.G2; ++o) {
-        const int wg = p.w3_groups > 1 ? o : 0;
-        uint64_t b[PARTS];
+    };
+    auto s3o = [&](int o) {
+      const int wg = p.w3_groups > 1 ? o : 0;
+      uint64_t bd[PARTS];
 #pragma unroll
-        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sw3 + (uint32_t)(j * p.w3_groups + wg) * p.w3_img, r3, c3, km, 0, 0);
-        mbar_wait(&bars.au_full, n_au & 1);
-        DL_PROF(11 + 3 * o);
-        ++n_au;
-        fence_after();
-        for (int kk = 0; kk < nk3; ++kk) {
-          if (elect_one()) kstep_ts<PARTS>(tbase + p.colD3, tbase + p.colA3 + 8u * kk, p.N2 / 2, b, id3, kk == 0);
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) b[j] += ks3;
-        }
-        if (elect_one()) commit(&bars.y_full);
+      for (int j = 0; j < PARTS; ++j) bd[j] = wdesc(sw3 + (uint32_t)(j * p.w3_groups + wg) * p.w3_img, c3, km, 0);
+      mbar_wait(&bars.au_full, n_au & 1);
+      ++n_au;
+      fence_after();
+      for (int kk = 0; kk < p.N2 / 16; ++kk) {
+        if (elect_one()) kstep_ts<PARTS>(tbase + p.colD3, tbase + p.colA3 + 8u * kk, p.N2 / 2, bd, id3, kk == 0);
         __syncwarp();
-        DL_PROF(12 + 3 * o);
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd[j] += ks3;
+      }
+      if (elect_one()) commit(&bars.y_full);
+      __syncwarp();
+    };
+    const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    if (p.overlap) {
+      // stage 1 of tile i+1 interleaved with stage 3 of tile i (their TMEM regions are disjoint)
+      if (nmine > 0) {
+        for (int g = 0; g < p.G1; ++g) s1g(0, g);
+        s2(0);
+      }
+      const int gmax = p.G1 > p.G2 ? p.G1 : p.G2;
+      for (uint32_t it = 0; it < nmine; ++it) {
+        for (int o = 0; o < gmax; ++o) {
+          if (it + 1 < nmine && o < p.G1) s1g(it + 1, o);
+          if (o < p.G2) s3o(o);
+        }
+        if (it + 1 < nmine) s2(it + 1);
+      }
+    } else {
+      for (uint32_t it = 0; it < nmine; ++it) {
+        for (int g = 0; g < p.G1; ++g) s1g(it, g);
+        s2(it);
+        for (int o = 0; o < p.G2; ++o) s3o(o);
       }
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == kEWarps) tmem_dealloc(tbase, 512);
+  if (warp == kWarpLD) tmem_dealloc(tbase, 512);
 }
 
-// ---------------------------------------------------------------------------- operand packing
-// `ng` row-major fp32 matrices of (nrb*rb) x (ncb*cb) -> PARTS bf16 images each of (nrb*rbp) x (ncb*cbp)
-// in the core-matrix blocked layout, image (q, g) at (q * ng + g) * img_elems.  Padding is zero.
-__global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, int ng, int nrb, int rb, int rbp,
-                       int ncb, int cb, int cbp, int parts) {
-  const int R = nrb * rbp, C = ncb * cbp;
-  const int64_t img = (int64_t)R * C;
-  const int64_t n = img * ng;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(e / img);
-    const int rc = (int)(e - (int64_t)g * img);
-    const int r = rc / C, c = rc - r * C;
-    const int bi = r / rbp, rr = r - bi * rbp, bj = c / cbp, cc = c - bj * cbp;
-    float v = 0.f;
-    if (rr < rb && cc < cb) v = __ldg(W + (int64_t)g * (nrb * rb) * (ncb * cb) + (int64_t)(bi * rb + rr) * (ncb * cb) + bj * cb + cc);
-    const int64_t off = ((int64_t)(r >> 3) * (C >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
-    for (int q = 0; q < parts; ++q) {
-      const uint32_t pk = pack_bf16x2(v, 0.f);
-      out[((int64_t)q * ng + g) * img + off] = (uint16_t)(pk & 0xFFFFu);
-      v -= bf16lo_to_f32(pk);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------- LSC weight Gram
+// ============================================================================ LSC weight Gram
 struct GramP {
   const float* x;
   const float* dy;
@@ -443,49 +447,52 @@ struct GramP {
   float* partials;           // [grid][GR*GC] then db [grid][S_out]
   int64_t nbatch, nvox, x_bs, dy_bs, tiles_per_b;
   int S_in, N, NPi, RPi, S_out, N_out, NPo, RPo, R_out;
-  int wM_groups;
+  int wM_groups, base_aligned;
+  int NS, NA;
   uint32_t wM_img, wB_img;
-  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_tab, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
-  uint32_t colGA, colGB, colGC, colA, colD;
+  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_ring, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
+  uint32_t colGA, colGB, colGC, colA, colDg, colDc;
   int GR, GC;                // g rows (S_out*RPo), c rows (S_in*RPi)
 };
 
-struct GBars {
-  uint64_t a_full, a_empty, d_full, tiles_full, gram_done;
+struct BarsG {
+  uint64_t ld_full[kMaxStages], ld_empty[kMaxStages], a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t dg_full, dg_free, dc_full, dc_free, tiles_full, gram_done;
   float db[4];
   uint32_t tmem_base;
 };
 
-// byte offset of (row j, voxel k) in a SWIZZLE_128B K-major tile with `rows` rows (K = 128 voxels)
-__device__ __forceinline__ uint32_t sw128_off(int j, int k, int rows) {
-  return (uint32_t)(k >> 6) * (uint32_t)(rows >> 3) * 1024u + (uint32_t)(j >> 3) * 1024u + (uint32_t)(j & 7) * 128u +
-         (uint32_t)((((k & 63) >> 3) ^ (j & 7)) << 4) + (uint32_t)(k & 7) * 2u;
-}
-
-template <int PARTS, int MAXC>
+template <int PARTS>
 __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  GBars& bars = *reinterpret_cast<GBars*>(smem + p.sm_bar);
+  BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kSlotW = PARTS * 8;
   {
     const uint32_t bM = (uint32_t)PARTS * p.wM_groups * p.wM_img, bB = (uint32_t)PARTS * p.wB_img;
-    const uint4* sM = reinterpret_cast<const uint4*>(p.wM);
-    const uint4* sB = reinterpret_cast<const uint4*>(p.wB);
-    uint4* dM = reinterpret_cast<uint4*>(smem + p.sm_wM);
-    uint4* dB = reinterpret_cast<uint4*>(smem + p.sm_wB);
+    const uint4 *sM = reinterpret_cast<const uint4*>(p.wM), *sB = reinterpret_cast<const uint4*>(p.wB);
+    uint4 *dM = reinterpret_cast<uint4*>(smem + p.sm_wM), *dB = reinterpret_cast<uint4*>(smem + p.sm_wB);
     for (uint32_t i = threadIdx.x; i < bM / 16; i += blockDim.x) dM[i] = __ldg(sM + i);
     for (uint32_t i = threadIdx.x; i < bB / 16; i += blockDim.x) dB[i] = __ldg(sB + i);
-    // zero both operand tiles once: padding rows/garbage rows must stay finite
+    // operand tiles (and the margin block C over-reads) start zeroed: padding rows stay finite
     uint4* z = reinterpret_cast<uint4*>(smem + p.sm_c);
-    const uint32_t zb = p.sm_bar - p.sm_c;
-    for (uint32_t i = threadIdx.x; i < zb / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < (p.sm_ring - p.sm_c) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
-  if (warp == kEWarps) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpLD) tmem_alloc(&bars.tmem_base, 512);
   if (threadIdx.x == 0) {
-    mbar_init(&bars.a_full, kEWarps);
-    mbar_init(&bars.a_empty, 1);
-    mbar_init(&bars.d_full, 1);
-    mbar_init(&bars.tiles_full, kEWarps);
+    for (int s = 0; s < p.NS; ++s) {
+      mbar_init(&bars.ld_full[s], 1);
+      mbar_init(&bars.ld_empty[s], kIN);
+    }
+    for (int s = 0; s < p.NA; ++s) {
+      mbar_init(&bars.a_full[s], kIN);
+      mbar_init(&bars.a_empty[s], 1);
+    }
+    mbar_init(&bars.dg_full, 1);
+    mbar_init(&bars.dg_free, kMID);
+    mbar_init(&bars.dc_full, 1);
+    mbar_init(&bars.dc_free, kMID);
+    mbar_init(&bars.tiles_full, kMID);
     mbar_init(&bars.gram_done, 1);
     for (int o = 0; o < 4; ++o) bars.db[o] = 0.f;
     mbar_fence_init();
@@ -496,142 +503,142 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
   fence_after();
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
+  const int nkg = p.NPo / 16, nkc = p.NPi / 16;
+  uint8_t* ring = smem + p.sm_ring;
 
-  if (warp < kEWarps) {
-    const int qd = warp & 3, cg = warp >> 2;
-    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
-    const int row = 32 * qd + lane;
-    float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t n_a = 0, n_d = 0, it = 0;
-    // one "item" = one group of one operand: items 0..S_out-1 are dy groups, S_out.. are x groups
-    auto load_group = [&](const float* base, int64_t bs, int C, int K, int64_t t, int g, float (&buf)[MAXC][16]) {
-      const int64_t b = t / p.tiles_per_b;
-      const int64_t v = (t - b * p.tiles_per_b) * kTileV + row;
-      const bool ok = v < p.nvox;
-      const float* src = base + b * bs + (int64_t)g * C * p.nvox + v;
-      const int nck = K / 16;
-#pragma unroll
-      for (int ci = 0; ci < MAXC; ++ci) {
-        const int ck = cg + ci * kEW;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = ck * 16 + i;
-          buf[ci][i] = (ck < nck && n < C && ok) ? __ldg(src + (int64_t)n * p.nvox) : 0.f;
+  // chunk sequence per tile: dy groups (S_out x nkg chunks), then x groups (S_in x nkc chunks)
+  if (warp == kWarpLD) {
+    uint32_t seq = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
+      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
+      for (int pass = 0; pass < 2; ++pass) {
+        const int G = pass ? p.S_in : p.S_out, C = pass ? p.N : p.N_out, nk = pass ? nkc : nkg;
+        for (int g = 0; g < G; ++g) {
+          const float* src = (pass ? p.x + b * p.x_bs : p.dy + b * p.dy_bs) + (int64_t)g * C * p.nvox + v0;
+          for (int k = 0; k < nk; ++k, ++seq) {
+            const uint32_t s = seq % p.NS;
+            if (seq >= (uint32_t)p.NS) mbar_wait(&bars.ld_empty[s], ((seq / p.NS) - 1) & 1);
+            load_chunk(ring + s * kChunkBytes, &bars.ld_full[s], src, C, k, p.nvox, safe);
+          }
         }
       }
-    };
-    auto put_a = [&](const float (&cur)[MAXC][16], int K) {
-      if (n_a > 0) mbar_wait(&bars.a_empty, (n_a - 1) & 1);
-      fence_after();
-      const int nck = K / 16;
-#pragma unroll
-      for (int ci = 0; ci < MAXC; ++ci) {
-        const int ck = cg + ci * kEW;
-        if (ck < nck) split_store16<PARTS>(tq + p.colA + (uint32_t)ck * 8, K / 2, cur[ci]);
+    }
+  } else if (warp < kIN) {
+    const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
+    const int row = 32 * warp + lane;
+    uint32_t seq = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
+      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
+      for (int pass = 0; pass < 2; ++pass) {
+        const int G = pass ? p.S_in : p.S_out, C = pass ? p.N : p.N_out, nk = pass ? nkc : nkg;
+        for (int g = 0; g < G; ++g) {
+          const float* src = (pass ? p.x + b * p.x_bs : p.dy + b * p.dy_bs) + (int64_t)g * C * p.nvox + v0;
+          for (int k = 0; k < nk; ++k, ++seq) {
+            const uint32_t s = seq % p.NS, a = seq % p.NA;
+            mbar_wait(&bars.ld_full[s], (seq / p.NS) & 1);
+            float v[16];
+            read_chunk(ring + s * kChunkBytes, src, C, k, p.nvox, v0, row, safe, v);
+            warp_arrive(&bars.ld_empty[s]);
+            if (seq >= (uint32_t)p.NA) mbar_wait(&bars.a_empty[a], ((seq / p.NA) - 1) & 1);
+            fence_after();
+            split_store16<PARTS>(tq + p.colA + a * kSlotW, 8, v);
+            tmem_wait_st();
+            fence_before();
+            warp_arrive(&bars.a_full[a]);
+          }
+        }
       }
-      tmem_wait_st();
-      fence_before();
-      warp_arrive(&bars.a_full);
-      ++n_a;
-    };
-    // D (fp32) -> two bf16 terms in the SW128 tile; for g also accumulate beta . g per output shell
-    auto drain = [&](uint32_t tile, int rows, int nch, bool is_g) {
-      mbar_wait(&bars.d_full, n_d & 1);
-      ++n_d;
+    }
+  } else if (warp < kWarpMMA) {
+    const int mw = warp - kIN, qd = mw & 3, cg = mw >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
+    const int row = 32 * qd + lane;
+    const int grow = p.GR < 128 ? 128 : p.GR;
+    float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      // ---- g -> two-term SW128 tile (+ beta . g for the bias gradient) ----
+      mbar_wait(&bars.dg_full, it & 1);
+      if (it > 0) mbar_wait(&bars.gram_done, (it - 1) & 1);   // previous Gram finished reading the tiles
       fence_after();
-      for (int ck = cg; ck < nch / 16; ck += kEW) {
+      for (int ck = cg; ck < p.GR / 16; ck += 2) {
         float vv[16];
-        ld16f(tq + p.colD + (uint32_t)ck * 16, vv);
+        ld16f(tq + p.colDg + (uint32_t)ck * 16, vv);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int j = ck * 16 + i;
-          if (is_g) {
-            const int o = j / p.RPo, r = j - o * p.RPo;
-            if (r < p.R_out && o < 4) dbacc[o] += __ldg(p.beta + r) * vv[i];
-          }
+          const int o = j / p.RPo, r = j - o * p.RPo;
+          if (r < p.R_out && o < 4) dbacc[o] += __ldg(p.beta + r) * vv[i];
           const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
-          const float rem = vv[i] - bf16lo_to_f32(pk0);
-          const uint32_t pk1 = pack_bf16x2(rem, 0.f);
-          const uint32_t off = sw128_off(j, row, rows);
-          *reinterpret_cast<uint16_t*>(smem + tile + off) = (uint16_t)pk0;
-          *reinterpret_cast<uint16_t*>(smem + tile + p.gtile * 0 + (is_g ? p.gtile : p.ctile) + off) = (uint16_t)pk1;
+          const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
+          const uint32_t off = sw128_off(j, row, grow);
+          *reinterpret_cast<uint16_t*>(smem + p.sm_g + off) = (uint16_t)pk0;
+          *reinterpret_cast<uint16_t*>(smem + p.sm_g + p.gtile + off) = (uint16_t)pk1;
         }
       }
-    };
-    float pf[MAXC][16];
-    int64_t t = blockIdx.x;
-    if (t < ntiles) load_group(p.dy, p.dy_bs, p.N_out, p.NPo, t, 0, pf);
-    for (; t < ntiles; t += gridDim.x, ++it) {
-      // ---- g = B'^T dy, one output shell at a time ----
-      for (int o = 0; o < p.S_out; ++o) {
-        float cur[MAXC][16];
-#pragma unroll
-        for (int ci = 0; ci < MAXC; ++ci)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) cur[ci][i] = pf[ci][i];
-        if (o + 1 < p.S_out) load_group(p.dy, p.dy_bs, p.N_out, p.NPo, t, o + 1, pf);
-        else load_group(p.x, p.x_bs, p.N, p.NPi, t, 0, pf);
-        put_a(cur, p.NPo);
-      }
-      if (it > 0) mbar_wait(&bars.gram_done, (it - 1) & 1);   // operand tiles free again
-      drain(p.sm_g, p.GR < 128 ? 128 : p.GR, p.GR, true);
-      // ---- c = M x, one input shell at a time ----
-      for (int s = 0; s < p.S_in; ++s) {
-        float cur[MAXC][16];
-#pragma unroll
-        for (int ci = 0; ci < MAXC; ++ci)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) cur[ci][i] = pf[ci][i];
-        if (s + 1 < p.S_in) load_group(p.x, p.x_bs, p.N, p.NPi, t, s + 1, pf);
-        else if (t + gridDim.x < ntiles) load_group(p.dy, p.dy_bs, p.N_out, p.NPo, t + gridDim.x, 0, pf);
-        put_a(cur, p.NPi);
-      }
-      drain(p.sm_c, p.GC, p.GC, false);
-      fence_proxy_async();
       fence_before();
+      warp_arrive(&bars.dg_free);
+      // ---- c -> two-term SW128 tile ----
+      mbar_wait(&bars.dc_full, it & 1);
+      fence_after();
+      for (int ck = cg; ck < p.GC / 16; ck += 2) {
+        float vv[16];
+        ld16f(tq + p.colDc + (uint32_t)ck * 16, vv);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = ck * 16 + i;
+          const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
+          const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
+          const uint32_t off = sw128_off(j, row, p.GC);
+          *reinterpret_cast<uint16_t*>(smem + p.sm_c + off) = (uint16_t)pk0;
+          *reinterpret_cast<uint16_t*>(smem + p.sm_c + p.ctile + off) = (uint16_t)pk1;
+        }
+      }
+      fence_before();
+      warp_arrive(&bars.dc_free);
+      fence_proxy_async();
       warp_arrive(&bars.tiles_full);
     }
     if (it > 0) mbar_wait(&bars.gram_done, (it - 1) & 1);
     fence_after();
-    // ---- write this CTA's Gram partial: G[j (g row)][i (c row)] ----
+    // ---- this CTA's Gram partial: G[j (g row)][i (c row)] ----
     float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
-    const int rA = row;  // block A: lane = g row
-    for (int ck = cg; ck < p.GC / 16; ck += kEW) {
+    for (int ck = cg; ck < p.GC / 16; ck += 2) {       // block A: lane = g row
       float vv[16];
       ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
-      if (rA < p.GR)
+      if (row < p.GR)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) part[(int64_t)rA * p.GC + ck * 16 + i] = vv[i];
+        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = vv[i];
     }
     if (p.GR > 128 && cg == 0) {
       float vv[16];
-      ld16f(tq + p.colGB, vv);   // block B: lane = c row i (< 128), col = g row 128 + c
+      ld16f(tq + p.colGB, vv);   // block B: lane = c row i (< 128), column = g row 128 + c
       if (row < p.GC)
 #pragma unroll
         for (int c = 0; c < 16; ++c)
           if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = vv[c];
       if (p.GC > 128 && qd == 0) {
-        ld16f(tq + p.colGC, vv);   // block C (M=64): lanes 0..15 = c rows 128..143
+        ld16f(tq + p.colGC, vv);   // block C (M = 64): lanes 0..15 = c rows 128..143
         if (lane < 16 && 128 + lane < p.GC)
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = vv[c];
       }
     }
-    // ---- db partial: sum over this CTA's voxels of beta . g[o] ----
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
       float s = dbacc[o];
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (lane == 0 && o < p.S_out) atomicAdd(&bars.db[o], s);
     }
-    named_sync(1, kEWarps * 32);
-    if (threadIdx.x == 0) {
+    named_sync(1, kMID * 32);
+    if (mw == 0 && lane == 0) {
       float* dbp = p.partials + (int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out;
       for (int o = 0; o < p.S_out; ++o) dbp[o] = bars.db[o];
     }
-  } else {
-    // =========================== MMA issuer (converged warp, one elected lane issues) ===========
+  } else if (warp == kWarpMMA) {
     const uint32_t sM = smem_u32(smem + p.sm_wM), sB = smem_u32(smem + p.sm_wB);
     const uint32_t sc = smem_u32(smem + p.sm_c), sg = smem_u32(smem + p.sm_g);
     const uint32_t idg = idesc_bf16(128, p.RPo, 0, 1);   // g: A = dy (TMEM), B = B' image MN-major
@@ -640,48 +647,37 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
     const int grow = p.GR < 128 ? 128 : p.GR;
     const uint32_t ASg = (uint32_t)(grow / 8) * 1024u, ASc = (uint32_t)(p.GC / 8) * 1024u;
     const uint64_t ksg = wkstep(p.RPo, 0), ksc = wkstep(p.NPi, 1);
-    const int nkg = p.NPo / 16, nkc = p.NPi / 16;
-    uint32_t n_a = 0, it = 0;
+    uint32_t seq = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      for (int o = 0; o < p.S_out; ++o) {
-        uint64_t b[PARTS];
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sB + (uint32_t)j * p.wB_img, p.NPo, p.RPo, 0, 0, 0);
-        mbar_wait(&bars.a_full, n_a & 1);
-        ++n_a;
-        fence_after();
-        const uint32_t d = tbase + p.colD + (uint32_t)(o * p.RPo);
-        for (int kk = 0; kk < nkg; ++kk) {
-          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA + 8u * kk, p.NPo / 2, b, idg, kk == 0);
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) b[j] += ksg;
+      for (int pass = 0; pass < 2; ++pass) {
+        if (it > 0) {
+          mbar_wait(pass ? &bars.dc_free : &bars.dg_free, (it - 1) & 1);
+          fence_after();
         }
-        if (elect_one()) commit(&bars.a_empty);
-        __syncwarp();
-      }
-      if (elect_one()) commit(&bars.d_full);
-      __syncwarp();
-      for (int s = 0; s < p.S_in; ++s) {
-        const int wg = p.wM_groups > 1 ? s : 0;
-        uint64_t b[PARTS];
+        const int G = pass ? p.S_in : p.S_out, nk = pass ? nkc : nkg;
+        for (int g = 0; g < G; ++g) {
+          uint64_t bd[PARTS];
+          const int wg = p.wM_groups > 1 ? g : 0;
 #pragma unroll
-        for (int j = 0; j < PARTS; ++j) b[j] = wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.RPi, p.NPi, 1, 0, 0);
-        mbar_wait(&bars.a_full, n_a & 1);
-        ++n_a;
-        fence_after();
-        const uint32_t d = tbase + p.colD + (uint32_t)(s * p.RPi);
-        for (int kk = 0; kk < nkc; ++kk) {
-          if (elect_one()) kstep_ts<PARTS>(d, tbase + p.colA + 8u * kk, p.NPi / 2, b, idc, kk == 0);
-          __syncwarp();
+          for (int j = 0; j < PARTS; ++j)
+            bd[j] = pass ? wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.NPi, 1, 0)
+                         : wdesc(sB + (uint32_t)j * p.wB_img, p.RPo, 0, 0);
+          const uint32_t d = tbase + (pass ? p.colDc + (uint32_t)(g * p.RPi) : p.colDg + (uint32_t)(g * p.RPo));
+          for (int k = 0; k < nk; ++k, ++seq) {
+            const uint32_t a = seq % p.NA;
+            mbar_wait(&bars.a_full[a], (seq / p.NA) & 1);
+            fence_after();
+            if (elect_one()) {
+              kstep_ts<PARTS>(d, tbase + p.colA + a * kSlotW, 8, bd, pass ? idc : idg, k == 0);
+              commit(&bars.a_empty[a]);
+              if (k == nk - 1 && g == G - 1) commit(pass ? &bars.dc_full : &bars.dg_full);
+            }
+            __syncwarp();
 #pragma unroll
-          for (int j = 0; j < PARTS; ++j) b[j] += ksc;
+            for (int j = 0; j < PARTS; ++j) bd[j] += pass ? ksc : ksg;
+          }
         }
-        if (elect_one()) commit(&bars.a_empty);
-        __syncwarp();
       }
-      if (elect_one()) commit(&bars.d_full);
-      __syncwarp();
       // ---- Gram over this tile's 128 voxels (two-term split operands, three blocks) ----
       mbar_wait(&bars.tiles_full, it & 1);
       fence_after();
@@ -710,10 +706,35 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
   }
   fence_before();
   __syncthreads();
-  if (warp == kEWarps) tmem_dealloc(tbase, 512);
+  if (warp == kWarpLD) tmem_dealloc(tbase, 512);
 }
 
-// fixed-order float64 reduction of the per-CTA Gram partials, then dW = <P_k, G_{o,s}>, db = sum of partials
+// ---------------------------------------------------------------------------- operand packing
+// `ng` row-major fp32 matrices of (nrb*rb) x (ncb*cb) -> PARTS bf16 images each of (nrb*rbp) x (ncb*cbp)
+// in the core-matrix blocked layout, image (q, g) at (q * ng + g) * img_elems.  Padding is zero.
+__global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, int ng, int nrb, int rb, int rbp,
+                       int ncb, int cb, int cbp, int parts) {
+  const int R = nrb * rbp, C = ncb * cbp;
+  const int64_t img = (int64_t)R * C;
+  const int64_t n = img * ng;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(e / img);
+    const int rc = (int)(e - (int64_t)g * img);
+    const int r = rc / C, c = rc - r * C;
+    const int bi = r / rbp, rr = r - bi * rbp, bj = c / cbp, cc = c - bj * cbp;
+    float v = 0.f;
+    if (rr < rb && cc < cb)
+      v = __ldg(W + (int64_t)g * (nrb * rb) * (ncb * cb) + (int64_t)(bi * rb + rr) * (ncb * cb) + bj * cb + cc);
+    const int64_t off = ((int64_t)(r >> 3) * (C >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+    for (int q = 0; q < parts; ++q) {
+      const uint32_t pk = pack_bf16x2(v, 0.f);
+      out[((int64_t)q * ng + g) * img + off] = (uint16_t)(pk & 0xFFFFu);
+      v -= bf16lo_to_f32(pk);
+    }
+  }
+}
+
+// fixed-order float64 reduction of the per-CTA Gram partials
 __global__ void gram_reduce_k(const float* __restrict__ partials, double* __restrict__ G, int nparts, int n) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -722,6 +743,7 @@ __global__ void gram_reduce_k(const float* __restrict__ partials, double* __rest
   }
 }
 
+// dW[o,s,k] = <P_k, G_{o,s}> and db[o] = sum of the per-CTA beta . g partials, in float64
 __global__ void gram_finalize_k(const double* __restrict__ G, const float* __restrict__ dbparts, int nparts,
                                 const float* __restrict__ P, float* __restrict__ dW, float* __restrict__ db, int s_out,
                                 int s_in, int K, int r_out, int r_in, int RPo, int RPi) {
@@ -747,8 +769,11 @@ __global__ void gram_finalize_k(const double* __restrict__ G, const float* __res
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if (threadIdx.x == 0) {
-      if (id < nw) { if (dW) dW[id] = (float)v; }
-      else if (db) db[id - nw] = (float)v;
+      if (id < nw) {
+        if (dW) dW[id] = (float)v;
+      } else if (db) {
+        db[id - nw] = (float)v;
+      }
     }
   }
 }
@@ -763,8 +788,8 @@ namespace {
 
 inline int r16(int64_t x) { return (int)((x + 15) / 16 * 16); }
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-long long* g_prof = nullptr;   // debug: phase timestamps of the next chain3 launch
+constexpr size_t kSmemMax = 227 * 1024;
+constexpr int kMaxParts = 256;
 
 int split_terms() {
   static int v = [] {
@@ -803,57 +828,65 @@ Dims make_dims(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r
 
 struct WsLayout {
   size_t imgM, imgL, imgB, parts, G, total;
-  uint32_t bM, bL, bB;   // bytes per image
-  int nparts;
 };
 
 WsLayout ws_layout(const Dims& d, int nparts) {
   WsLayout w;
-  w.bM = (uint32_t)(d.RPi * d.NPi * 2);
-  w.bL = (uint32_t)((d.s_out * d.RPo) * (d.s_in * d.RPi) * 2);
-  w.bB = (uint32_t)(d.NPo * d.RPo * 2);
-  const int GR = d.s_out * d.RPo, GC = d.s_in * d.RPi;
+  const size_t bM = (size_t)d.RPi * d.NPi * 2, bL = (size_t)(d.s_out * d.RPo) * (d.s_in * d.RPi) * 2,
+               bB = (size_t)d.NPo * d.RPo * 2;
+  const size_t GR = (size_t)d.s_out * d.RPo, GC = (size_t)d.s_in * d.RPi;
   size_t o = 0;
-  w.imgM = o; o = al(o + (size_t)3 * d.mg * w.bM, 256);
-  w.imgL = o; o = al(o + (size_t)3 * w.bL, 256);
-  w.imgB = o; o = al(o + (size_t)3 * w.bB, 256);
-  w.parts = o; o = al(o + (size_t)nparts * ((size_t)GR * GC + d.s_out) * 4, 256);
-  w.G = o; o = al(o + (size_t)GR * GC * 8, 256);
+  w.imgM = o; o = al(o + 3 * d.mg * bM, 256);
+  w.imgL = o; o = al(o + 3 * bL, 256);
+  w.imgB = o; o = al(o + 3 * bB, 256);
+  w.parts = o; o = al(o + (size_t)nparts * (GR * GC + d.s_out) * 4, 256);
+  w.G = o; o = al(o + GR * GC * 8, 256);
   w.total = o;
-  w.nparts = nparts;
   return w;
 }
 
-constexpr int kMaxParts = 256;
-
-// TMEM / smem plan for one chain3 direction; returns false if it does not fit.
-bool plan_chain3(Chain3& p, int parts) {
-  const int A1 = parts * p.K1 / 2, D1 = p.G1 * p.N1, A2 = parts * D1 / 2, D2 = p.G2 * p.N2, A3 = parts * p.N2 / 2;
-  if (p.N1 > 256 || p.N2 > 256 || p.N3 > 256 || p.G2 > 4 || (p.K1 / 16 + kEW - 1) / kEW > 8) return false;
-  p.colA1 = 0;
-  p.colD1 = A1;
-  p.colA2 = A1 + D1;
-  p.colD2 = 0;
-  // D2 reuses [0, ...) once stage 1 is drained; it must not overlap A2 (read by stage-2 MMAs).
-  if ((int)p.colA2 + A2 > 512 || D2 > (int)p.colA2 || D1 > 512) return false;
-  p.d3_sync = 0;
-  if (D2 + A3 <= (int)p.colA2) {
-    // A3 right after D2 (below A2); D3 after A2, or over A2 once all stage-2 MMAs completed
-    p.colA3 = D2;
-    if ((int)p.colA2 + A2 + p.N3 <= 512) {
-      p.colD3 = p.colA2 + A2;
-    } else if (D2 + A3 + p.N3 <= 512) {
-      p.colD3 = D2 + A3;
-      p.d3_sync = 1;
-    } else {
-      return false;
+// TMEM / shared-memory plan for one chain3 direction; false if it does not fit.
+// Regions: A slots | D1 | A2 | D2 (+ A3, D3).  Lifetimes inside a tile: D1 until A2 is built, A2 until
+// the stage-2 MMAs finish, D2 through the last stage-3 read, A3/D3 during stage 3.  A3/D3 may reuse
+// a dead region (A2 or D1) but never D2 or the A slots.  "overlap": D1/slots are free as soon as A2 is
+// built, so the next tile's stage 1 runs during this tile's stage 3.  free_at tells MID when to
+// release D1 (0: after A2 is built, 1: after the last D2 read, 2: after the last D3 read).
+bool plan_tmem(Chain3& p, int parts) {
+  const int slotw = parts * 8, D1w = p.G1 * p.N1, A2w = parts * D1w / 2, D2w = p.G2 * p.N2, A3w = parts * p.N2 / 2,
+            D3w = p.N3, S3 = A3w + D3w;
+  for (int na = 4; na >= 2; --na) {
+    p.NA = na;
+    p.colA = 0;
+    p.colD1 = na * slotw;
+    p.colA2 = p.colD1 + D1w;
+    if ((int)p.colA2 + A2w > 512) continue;
+    // overlap layouts: D2 after A2; stage 3 inside A2 or after D2
+    const int d2 = p.colA2 + A2w;
+    if (d2 + D2w <= 512) {
+      p.colD2 = d2;
+      p.overlap = 1;
+      p.free_at = 0;
+      if (S3 <= A2w) { p.colA3 = p.colA2; p.colD3 = p.colA2 + A3w; return true; }
+      if (d2 + D2w + S3 <= 512) { p.colA3 = d2 + D2w; p.colD3 = p.colA3 + A3w; return true; }
+      // compact variant of the same D2 placement: stage 3 in the (dead, contiguous) D1 + A2 regions
+      if (S3 <= D1w + A2w) { p.overlap = 0; p.free_at = 2; p.colA3 = p.colD1; p.colD3 = p.colD1 + A3w; return true; }
     }
-  } else if ((int)p.colA2 + A2 + A3 + p.N3 <= 512) {
-    p.colA3 = p.colA2 + A2;  // both stage-3 buffers above A2
-    p.colD3 = p.colA3 + A3;
-  } else {
-    return false;
+    // compact: D2 aliases D1, stage 3 inside A2
+    if (D2w <= D1w && S3 <= A2w) {
+      p.colD2 = p.colD1;
+      p.overlap = 0;
+      p.free_at = 1;
+      p.colA3 = p.colA2;
+      p.colD3 = p.colA2 + A3w;
+      return true;
+    }
   }
+  return false;
+}
+
+bool plan_chain3(Chain3& p, int parts) {
+  if (p.N1 > 256 || p.N2 > 256 || p.N3 > 256 || p.G1 * p.N1 > 512) return false;
+  if (!plan_tmem(p, parts)) return false;
   p.w1_img = (uint32_t)(p.N1 * p.K1 * 2);
   p.w2_img = (uint32_t)((p.G2 * p.N2) * (p.G1 * p.N1) * 2);
   p.w3_img = (uint32_t)(p.N3 * p.N2 * 2);
@@ -861,31 +894,32 @@ bool plan_chain3(Chain3& p, int parts) {
   p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
   p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
   p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
-  {
-    const int np = parts * (parts + 1) / 2, NT2 = p.G2 * p.N2;
-    const int n2g = NT2 <= 256 ? 1 : p.G2;
-    const size_t ents = (size_t)np * (p.G1 * (p.K1 / 16) + n2g * (p.G1 * p.N1 / 16) + p.G2 * (p.N2 / 16));
-    p.sm_tab = (uint32_t)o; o = al(o + ents * 16, 16);
-  }
-  p.sm_bar = (uint32_t)o; o = al(o + sizeof(Bars), 16);
+  p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 16);
+  const size_t fixed = o + al(sizeof(Bars3), 16);
+  if (fixed + 2 * kChunkBytes > kSmemMax) return false;
+  p.NS = (int)((kSmemMax - fixed) / kChunkBytes);
+  if (p.NS > kMaxStages) p.NS = kMaxStages;
+  p.sm_ring = (uint32_t)o; o = al(o + (size_t)p.NS * kChunkBytes, 16);
+  p.sm_bar = (uint32_t)o; o = al(o + sizeof(Bars3), 16);
   p.smem_bytes = (uint32_t)o;
-  return o <= 227 * 1024;
+  return o <= kSmemMax;
 }
 
 bool plan_gram(GramP& p, int parts) {
   p.GR = p.S_out * p.RPo;
   p.GC = p.S_in * p.RPi;
   if (p.GR > 144 || p.GC > 144 || p.S_out > 4) return false;
-  const int grow = p.GR < 128 ? 128 : p.GR;
+  const int grow = p.GR < 128 ? 128 : p.GR, slotw = parts * 8;
   p.colGA = 0;
   p.colGB = p.GC;
   p.colGC = p.GC + 16;
-  p.colA = p.GC + 32;
-  const int amax = parts * (p.NPo > p.NPi ? p.NPo : p.NPi) / 2;
-  p.colD = p.colA + amax;
-  const int dmax = p.GR > p.GC ? p.GR : p.GC;
-  if ((int)p.colD + dmax > 512) return false;
-  if ((p.NPo / 16 + kEW - 1) / kEW > 8 || (p.NPi / 16 + kEW - 1) / kEW > 8) return false;
+  const int col = p.GC + 32;
+  p.NA = (512 - col - p.GR - p.GC) / slotw;
+  if (p.NA > kMaxSlots) p.NA = kMaxSlots;
+  if (p.NA < 2) return false;
+  p.colA = col;
+  p.colDg = p.colA + p.NA * slotw;
+  p.colDc = p.colDg + p.GR;
   p.wM_img = (uint32_t)(p.RPi * p.NPi * 2);
   p.wB_img = (uint32_t)(p.NPo * p.RPo * 2);
   p.ctile = (uint32_t)(p.GC / 8) * 1024u * 2u;
@@ -895,53 +929,31 @@ bool plan_gram(GramP& p, int parts) {
   p.sm_wB = (uint32_t)o; o = al(o + (size_t)parts * p.wB_img, 1024);
   p.sm_c = (uint32_t)o; o = al(o + (size_t)2 * p.ctile, 1024);
   p.sm_g = (uint32_t)o; o = al(o + (size_t)2 * p.gtile, 1024);
-  // block C reads c rows up to 191 of every K-atom: keep >= 8 KB of mapped smem after the g tile
-  o = al(o + 8192, 1024);
-  {
-    const int np = parts * (parts + 1) / 2;
-    const size_t ts = (size_t)np * (p.S_out * (p.NPo / 16) + p.S_in * (p.NPi / 16)) * 16;
-    p.sm_tab = (uint32_t)o; o = al(o + ts + (size_t)(kTileV / 16) * 3 * 3 * sizeof(SsEnt), 16);
-  }
-  p.sm_bar = (uint32_t)o; o = al(o + sizeof(GBars), 16);
+  o = al(o + 8192, 1024);   // block C reads c rows up to 191 of every K-atom: keep mapped smem after g
+  const size_t fixed = o + al(sizeof(BarsG), 16);
+  if (fixed + 2 * kChunkBytes > kSmemMax) return false;
+  p.NS = (int)((kSmemMax - fixed) / kChunkBytes);
+  if (p.NS > kMaxStages) p.NS = kMaxStages;
+  p.sm_ring = (uint32_t)o; o = al(o + (size_t)p.NS * kChunkBytes, 16);
+  p.sm_bar = (uint32_t)o; o = al(o + sizeof(BarsG), 16);
   p.smem_bytes = (uint32_t)o;
-  return o <= 227 * 1024;
+  return o <= kSmemMax;
 }
 
-template <int PARTS, int MAXC>
-int run_chain3_t(const Chain3& p, int grid, cudaStream_t st) {
-  auto k = chain3_tc<PARTS, MAXC>;
+template <int PARTS>
+int run_chain3(const Chain3& p, int grid, cudaStream_t st) {
+  auto k = chain3_tc<PARTS>;
   DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
   k<<<grid, kThreads, p.smem_bytes, st>>>(p);
   return after_launch("chain3_tc");
 }
 
 template <int PARTS>
-int run_chain3_p(const Chain3& p, int grid, cudaStream_t st) {
-  const int mc = (p.K1 / 16 + kEW - 1) / kEW;
-  if (mc <= 1) return run_chain3_t<PARTS, 1>(p, grid, st);
-  if (mc <= 2) return run_chain3_t<PARTS, 2>(p, grid, st);
-  if (mc <= 3) return run_chain3_t<PARTS, 3>(p, grid, st);
-  if (mc <= 4) return run_chain3_t<PARTS, 4>(p, grid, st);
-  return run_chain3_t<PARTS, 8>(p, grid, st);
-}
-
-template <int PARTS, int MAXC>
-int run_gram_t(const GramP& p, int grid, cudaStream_t st) {
-  auto k = gram_tc<PARTS, MAXC>;
+int run_gram(const GramP& p, int grid, cudaStream_t st) {
+  auto k = gram_tc<PARTS>;
   DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
   k<<<grid, kThreads, p.smem_bytes, st>>>(p);
   return after_launch("gram_tc");
-}
-
-template <int PARTS>
-int run_gram_p(const GramP& p, int grid, cudaStream_t st) {
-  const int kmax = p.NPo > p.NPi ? p.NPo : p.NPi;
-  const int mc = (kmax / 16 + kEW - 1) / kEW;
-  if (mc <= 1) return run_gram_t<PARTS, 1>(p, grid, st);
-  if (mc <= 2) return run_gram_t<PARTS, 2>(p, grid, st);
-  if (mc <= 3) return run_gram_t<PARTS, 3>(p, grid, st);
-  if (mc <= 4) return run_gram_t<PARTS, 4>(p, grid, st);
-  return run_gram_t<PARTS, 8>(p, grid, st);
 }
 
 int pack(const float* W, uint16_t* out, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp, int parts,
@@ -1015,15 +1027,13 @@ bool chain_fits(const Dims& d) {
 
 int grid_for(int64_t ntiles, int sm) { return (int)(ntiles < sm ? (ntiles > 0 ? ntiles : 1) : sm); }
 
+int aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0 ? 1 : 0; }
+
 }  // namespace
 }  // namespace tc
 }  // namespace dl
 
 extern "C" {
-
-// Debug hook (not part of the documented ABI): record chain3 phase timestamps into `buf`
-// (device, >= 8*2*32 int64) on subsequent forward launches; NULL disables.
-void dl_debug_chain_prof(void* buf) { dl::tc::g_prof = reinterpret_cast<long long*>(buf); }
 
 int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
                        int m_per_shell) {
@@ -1060,9 +1070,9 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   p.in = x;
   p.out = y;
   p.bias2 = bvec;
-  p.prof = g_prof;
+  p.base_aligned = aligned16(x);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
-  return d.parts == 3 ? run_chain3_p<3>(p, grid, st) : run_chain3_p<2>(p, grid, st);
+  return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
 }
 
 int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, float* db, const float* M, int m_per_shell,
@@ -1088,8 +1098,9 @@ int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, floa
     p.in = dy;
     p.out = dx;
     p.bias2 = nullptr;
+    p.base_aligned = aligned16(dy);
     const int grid = grid_for(ntiles, sm);
-    DL_TRY(d.parts == 3 ? run_chain3_p<3>(p, grid, st) : run_chain3_p<2>(p, grid, st));
+    DL_TRY(d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st));
   }
   if (dW || db) {
     GramP g = gram_params(d, w, ws);
@@ -1100,8 +1111,9 @@ int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, floa
       g.x = x;
       g.dy = dy;
       g.beta = beta;
+      g.base_aligned = aligned16(x) && aligned16(dy);
       nparts = grid_for(ntiles, sm < kMaxParts ? sm : kMaxParts);
-      DL_TRY(d.parts == 3 ? run_gram_p<3>(g, nparts, st) : run_gram_p<2>(g, nparts, st));
+      DL_TRY(d.parts == 3 ? run_gram<3>(g, nparts, st) : run_gram<2>(g, nparts, st));
     }
     float* partials = reinterpret_cast<float*>(ws + w.parts);
     double* G = reinterpret_cast<double*>(ws + w.G);
