@@ -5,9 +5,11 @@
 // fitting.sh_to_signal (fitting.py:239-250); the backward is the adjoint (SPEC.md:12 leaves it out).
 //
 // One persistent CTA per SM walks voxel tiles of 128 (= the MMA M dimension), warp-specialised:
-//   warp 13      TMA loader: 1-D bulk copies (cp.async.bulk) of 16-channel x 128-voxel row blocks
-//                into a shared-memory ring (rows are copied from the 16-byte aligned address below
-//                the tile start, so any voxel count works; the shift is stored beside the rows);
+//   warp 13      loader: TMA tensor copies (cp.async.bulk.tensor) of 16-channel x 128-voxel blocks into
+//                a shared-memory ring.  The input is viewed as pairs of channel rows, so one 3-D tensor
+//                map serves any even voxel count; each block is two 8-row boxes (even / odd channels).
+//                Shapes the map cannot describe (odd voxel or channel counts, unaligned pointers) fall
+//                back to per-warp 4-byte cp.async rings run by the IN warps themselves;
 //   warps 0-3    IN: thread t owns voxel t; reads its 16 values, splits each fp32 into PARTS bf16
 //                terms and writes them into a TMEM A-operand slot (lane = voxel);
 //   warp 12      MMA: one elected lane issues tcgen05.mma kind::f16 (A from TMEM, B = weights
@@ -20,6 +22,8 @@
 // tile's stage 1 is interleaved with this tile's stage 3.
 // gram: g = B'^T dy and c = M x on the tensor cores, staged as two-term bf16 SWIZZLE_128B tiles,
 // G = sum_v g c^T accumulated in TMEM for the whole CTA, then a float64 finalize dW = <P_k, G>.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -32,15 +36,15 @@ namespace tc {
 using namespace dl::umma;
 
 constexpr int kTileV = 128;                 // voxels per tile (MMA M)
-constexpr int kIN = 4;                      // input-conversion warps (one per TMEM lane quadrant)
-constexpr int kMID = 8;                     // epilogue warps (two per quadrant)
-constexpr int kWarpMMA = kIN + kMID;        // 12
-constexpr int kWarpLD = kWarpMMA + 1;       // 13
+constexpr int kIN = 4;                      // input warps (one per TMEM lane quadrant)
+constexpr int kMID = 8;                     // accumulator warps (two per quadrant, alternate columns)
+constexpr int kWarpMMA = kIN + kMID;        // 12: MMA issuer, also owns the TMEM allocation
+constexpr int kWarpLD = kWarpMMA + 1;       // 13: TMA loader
 constexpr int kThreads = (kWarpLD + 1) * 32;
-constexpr int kRowBytes = 528;              // 128 voxels + <= 3 floats of alignment shift, 16-B multiple
-constexpr int kChunkBytes = 16 * kRowBytes + 64;   // 16 rows + their 16 shifts
-constexpr int kMaxStages = 8;
+constexpr int kBoxV = kTileV + 4;           // TMA box width: 128 voxels + a 16-byte realignment margin
+constexpr int kStageBytes = 16 * kBoxV * 4; // one ring stage: 16 channels x 132 voxels fp32
 constexpr int kMaxSlots = 6;
+constexpr int kMaxStages = 8;
 
 // ---------------------------------------------------------------------------- small helpers
 template <int P> struct Pairs;
@@ -113,64 +117,159 @@ __device__ __forceinline__ uint32_t sw128_off(int j, int k, int rows) {
          (uint32_t)((((k & 63) >> 3) ^ (j & 7)) << 4) + (uint32_t)(k & 7) * 2u;
 }
 
-// A tile is "safe" for the bulk loader when every copied row (<= 132 floats from the aligned
-// address below the tile start) stays inside the tensor.
-__device__ __forceinline__ bool tile_safe(int64_t b, int64_t v0, int64_t nvox, int base_aligned) {
-  return v0 + kTileV + 4 <= nvox && (v0 >= 4 || b > 0 || base_aligned);
-}
-
-// ---------------------------------------------------------------------------- loader (one warp)
-// Bulk copies of the 16-row chunk `k` of one channel group (C real channels, src already offset
-// to the tile's first voxel) into a ring stage; unsafe tiles only arrive (IN loads directly).
-__device__ __forceinline__ void load_chunk(uint8_t* stage_ptr, uint64_t* full, const float* src_g, int C, int k,
-                                           int64_t nvox, bool safe) {
-  const int lane = threadIdx.x & 31;
-  if (!safe) {
-    if (lane == 0) mbar_arrive(full);
-    __syncwarp();
-    return;
-  }
-  const int c = 16 * k + lane;
-  const bool valid = lane < 16 && c < C;
-  uint32_t bytes = 0, shift = 0;
-  const float* a = nullptr;
-  if (valid) {
-    const float* row = src_g + (int64_t)c * nvox;
-    shift = (uint32_t)((reinterpret_cast<uintptr_t>(row) >> 2) & 3u);
-    a = row - shift;
-    bytes = ((128u + shift) * 4u + 15u) & ~15u;
-  }
-  if (lane < 16) reinterpret_cast<uint32_t*>(stage_ptr + 16 * kRowBytes)[lane] = shift;
-  uint32_t total = bytes;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
-  __syncwarp();
-  if (lane == 0) mbar_arrive_tx(full, total);
-  __syncwarp();
-  if (valid) bulk_g2s(stage_ptr + lane * kRowBytes, a, bytes, full);
-  __syncwarp();
-}
-
-// 16 channel values of this thread's voxel from a staged chunk (or directly from HBM for unsafe tiles)
-__device__ __forceinline__ void read_chunk(const uint8_t* stage_ptr, const float* src_g, int C, int k, int64_t nvox,
-                                           int64_t v0, int row, bool safe, float (&v)[16]) {
-  if (safe) {
-    const uint32_t* sh = reinterpret_cast<const uint32_t*>(stage_ptr + 16 * kRowBytes);
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      v[r] = (16 * k + r < C) ? reinterpret_cast<const float*>(stage_ptr + r * kRowBytes)[sh[r] + row] : 0.f;
-  } else {
-    const bool ok = v0 + row < nvox;
+// 16 rows (channels) of one voxel via 4-byte cp.async: rows < nval copy, the rest are zero-filled.
+__device__ __forceinline__ void stream_chunk(float* dst, const float* src, int64_t stride, int nval,
+                                             const float* dummy) {
+  if (nval >= 16) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const int c = 16 * k + r;
-      v[r] = (c < C && ok) ? __ldg(src_g + (int64_t)c * nvox + row) : 0.f;
+      cp_async4(dst + r * 32, src, 4u);
+      src += stride;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const bool valid = r < nval;
+      cp_async4(dst + r * 32, valid ? src : dummy, valid ? 4u : 0u);
+      src += stride;
+    }
+  }
+}
+
+// Hands one voxel's 16 values (split into PARTS bf16 terms) to the MMA warp through TMEM A slot
+// (aslot, around); advances the slot cursor.
+template <int PARTS>
+__device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int NA, uint64_t* a_full,
+                                      uint64_t* a_empty, uint32_t& aslot, uint32_t& around) {
+  if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
+  fence_after();
+  split_store16<PARTS>(tslots + aslot * (PARTS * 8), 8, v);
+  tmem_wait_st();
+  fence_before();
+  warp_arrive(&a_full[aslot]);
+  if (++aslot == (uint32_t)NA) {
+    aslot = 0;
+    ++around;
+  }
+}
+
+// Chunk r of a tile (the geometry functor): which input tensor, its first channel, and how many of
+// the 16 rows are real channels of the current group (the rest are zeroed).
+struct ChunkGeo {
+  int tensor, c0, nval;
+};
+
+// Fallback IN role (no tensor map): each warp streams its own 32-voxel segment of every chunk through
+// a private NS-deep ring with 4-byte cp.async (any alignment).  Every thread only reads back what it
+// copied itself, so cp.async.wait_group is the only synchronisation.
+template <int PARTS, int NS, typename Geo>
+__device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
+                                                int64_t nvox, const float* const (&base)[2], const int64_t (&bs)[2],
+                                                uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
+                                                float* ring) {
+  const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int64_t nmine = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * per_tile;
+  int64_t qp = 0;
+  uint32_t pslot = 0, cslot = 0, aslot = 0, around = 0;
+  auto issue = [&]() {
+    if (qp < total) {
+      const int64_t ti = qp / per_tile;
+      const int r = (int)(qp - ti * per_tile);
+      const int64_t t = blockIdx.x + ti * gridDim.x, b = t / tiles_per_b;
+      const int64_t v = (t - b * tiles_per_b) * kTileV + 32 * qd + lane;
+      const ChunkGeo cg = geo(r);
+      const bool vok = v < nvox;
+      const float* src = base[cg.tensor] + b * bs[cg.tensor] + (int64_t)cg.c0 * nvox + (vok ? v : 0);
+      stream_chunk(ring + pslot * 512 + lane, src, nvox, vok ? cg.nval : 0, base[0]);
+      ++qp;
+    }
+    cp_async_commit();
+    pslot = pslot + 1 == NS ? 0 : pslot + 1;
+  };
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) issue();
+  for (int64_t q = 0; q < total; ++q) {
+    issue();
+    cp_async_wait<NS - 1>();
+    float v[16];
+    const float* rp = ring + cslot * 512 + lane;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = rp[r * 32];
+    cslot = cslot + 1 == NS ? 0 : cslot + 1;
+    put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around);
+  }
+  cp_async_wait<0>();
+}
+
+// TMA loader (one warp, one elected lane issues): chunk (tile, r) -> ring stage, as two 8 x 132 boxes of
+// the channel-pair view (even channels first, then odd).  A box must start 16-byte aligned in global
+// memory; odd channel rows start at voxel offset nvox, so when nvox % 4 == 2 their box starts 2 voxels
+// early (shift) and the readers skip those.
+template <int NS, typename Geo>
+__device__ __forceinline__ void tma_loader(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
+                                           int64_t nvox, const CUtensorMap* maps, uint8_t* ring, uint64_t* full,
+                                           uint64_t* empty) {
+  if (elect_one()) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(maps) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(maps + 1) : "memory");
+  }
+  __syncwarp();
+  uint32_t s = 0, round = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t b = t / tiles_per_b;
+    const int v0 = (int)((t - b * tiles_per_b) * kTileV);
+    for (int r = 0; r < per_tile; ++r) {
+      const ChunkGeo cg = geo(r);
+      if (round > 0) mbar_wait_warp(&empty[s], (round - 1) & 1);
+      if (elect_one()) {
+        uint8_t* dst = ring + s * kStageBytes;
+        mbar_arrive_tx(&full[s], kStageBytes);
+        tma_load_3d(dst, maps + cg.tensor, v0, cg.c0 >> 1, (int)b, &full[s]);
+        tma_load_3d(dst + kStageBytes / 2, maps + cg.tensor, (int)nvox + v0 - (int)(nvox & 3), cg.c0 >> 1, (int)b,
+                    &full[s]);
+      }
+      __syncwarp();
+      if (++s == NS) {
+        s = 0;
+        ++round;
+      }
+    }
+  }
+}
+
+// IN role over the TMA ring: thread = voxel; row j of the chunk is channel-pair row j/2 of box j%2.
+template <int PARTS, int NS, typename Geo>
+__device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
+                                            int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
+                                            const float* ring, uint64_t* full, uint64_t* empty) {
+  const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int odd0 = 8 * kBoxV + (int)(nvox & 3);   // first odd-channel value of this thread, minus its voxel
+  uint32_t s = 0, round = 0, aslot = 0, around = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t b = t / tiles_per_b;
+    const bool vok = (t - b * tiles_per_b) * kTileV + 32 * qd + lane < nvox;
+    for (int r = 0; r < per_tile; ++r) {
+      const ChunkGeo cg = geo(r);
+      const int nval = vok ? cg.nval : 0;   // the odd-channel box reads past nvox into the next row
+      mbar_wait_warp(&full[s], round & 1);
+      const float* rp = ring + s * (kStageBytes / 4) + 32 * qd + lane;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = j < nval ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+      warp_arrive(&empty[s]);
+      if (++s == NS) {
+        s = 0;
+        ++round;
+      }
+      put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around);
     }
   }
 }
 
 // ============================================================================ chain3 kernel
 struct Chain3 {
+  CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
   const float* in;
   float* out;
   const float* bias2;                 // real stage-2 bias per (group, channel < C2) or null
@@ -182,21 +281,30 @@ struct Chain3 {
   int G2, C2, N2;                     // stage 2: groups, real out-ch/group, padded N
   int C3, N3;                         // stage 3: real / padded out-ch per group
   int w1_groups, w3_groups;
-  int adjoint, overlap, free_at, base_aligned;
-  int NS, NA;                         // loader ring stages, TMEM A slots
+  int adjoint, overlap, free_at, tma;
+  int NA, ns;                         // TMEM A slots, ring depth
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
   uint32_t colA, colD1, colA2, colD2, colA3, colD3;
+  long long* prof;                    // debug: per-role phase timestamps of CTA 0 (dl_debug_chain_prof)
 };
 
+// role r (0 IN, 1 MID, 2 MMA, 3 loader), tile it < 8, event ev < 32
+#define DL_PROF(r, ev)                                                                   \
+  do {                                                                                   \
+    if (p.prof && blockIdx.x == 0 && it < 8 && (threadIdx.x & 31) == 0)                  \
+      p.prof[((it)*4 + (r)) * 32 + (ev)] = clock64();                                    \
+  } while (0)
+
 struct Bars3 {
-  uint64_t ld_full[kMaxStages], ld_empty[kMaxStages], a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t full[kMaxStages], empty[kMaxStages];   // TMA ring
+  uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t d1_full, d1_free, ac_full, u_full, au_full, y_full;
   uint32_t tmem_base;
 };
 
-template <int PARTS>
-__global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
+template <int PARTS, int NS>
+__global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__ Chain3 p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   Bars3& bars = *reinterpret_cast<Bars3*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -218,14 +326,14 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
       sb[i] = (p.bias2 && r < p.C2) ? __ldg(p.bias2 + o * p.C2 + r) : 0.f;
     }
   }
-  if (warp == kWarpLD) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpMMA) tmem_alloc(&bars.tmem_base, 512);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.NS; ++s) {
-      mbar_init(&bars.ld_full[s], 1);
-      mbar_init(&bars.ld_empty[s], kIN);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], kIN);
     }
     for (int s = 0; s < p.NA; ++s) {
-      mbar_init(&bars.a_full[s], kIN);
+      mbar_init(&bars.a_full[s], 4);   // one arrival per TMEM lane quadrant
       mbar_init(&bars.a_empty[s], 1);
     }
     mbar_init(&bars.d1_full, 1);
@@ -243,60 +351,44 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
   const int nk1 = p.K1 / 16;
-  uint8_t* ring = smem + p.sm_ring;
+  const int per_tile = p.G1 * nk1;
+  auto geo = [&](int r) {
+    const int g = r / nk1, k = r - g * nk1;
+    return ChunkGeo{0, g * p.C1 + 16 * k, p.C1 - 16 * k};
+  };
 
-  if (warp == kWarpLD) {
-    // =========================== TMA loader ===========================
-    uint32_t seq = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
-      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
-      for (int g = 0; g < p.G1; ++g) {
-        const float* src = p.in + b * p.in_bs + (int64_t)g * p.C1 * p.nvox + v0;
-        for (int k = 0; k < nk1; ++k, ++seq) {
-          const uint32_t s = seq % p.NS;
-          if (seq >= (uint32_t)p.NS) mbar_wait(&bars.ld_empty[s], ((seq / p.NS) - 1) & 1);
-          load_chunk(ring + s * kChunkBytes, &bars.ld_full[s], src, p.C1, k, p.nvox, safe);
-        }
-      }
-    }
-  } else if (warp < kIN) {
-    // =========================== IN: staged rows -> split -> TMEM A slots ===========================
-    const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
-    const int row = 32 * warp + lane;
-    uint32_t seq = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
-      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
-      for (int g = 0; g < p.G1; ++g) {
-        const float* src = p.in + b * p.in_bs + (int64_t)g * p.C1 * p.nvox + v0;
-        for (int k = 0; k < nk1; ++k, ++seq) {
-          const uint32_t s = seq % p.NS, a = seq % p.NA;
-          mbar_wait(&bars.ld_full[s], (seq / p.NS) & 1);
-          float v[16];
-          read_chunk(ring + s * kChunkBytes, src, p.C1, k, p.nvox, v0, row, safe, v);
-          warp_arrive(&bars.ld_empty[s]);
-          if (seq >= (uint32_t)p.NA) mbar_wait(&bars.a_empty[a], ((seq / p.NA) - 1) & 1);
-          fence_after();
-          split_store16<PARTS>(tq + p.colA + a * kSlotW, 8, v);
-          tmem_wait_st();
-          fence_before();
-          warp_arrive(&bars.a_full[a]);
-        }
-      }
+  if (warp < kIN) {
+    // =========================== IN: ring -> split -> TMEM A slots ===========================
+    const uint32_t tslots = tbase + ((uint32_t)(32 * warp) << 16) + p.colA;
+    if (p.tma) {
+      in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
+                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty);
+    } else {
+      const float* const base[2] = {p.in, p.in};
+      const int64_t bs[2] = {p.in_bs, p.in_bs};
+      in_role_cpasync<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots, p.NA, bars.a_full,
+                                 bars.a_empty, reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
     }
   } else if (warp < kWarpMMA) {
-    // =========================== MID: accumulators -> next A / HBM ===========================
+    // =========================== MID: D1 -> A2, D2 (+bias) -> A3, D3 -> HBM ===========================
+    // two warps per TMEM lane quadrant, alternate 16-column chunks
     const int mw = warp - kIN, qd = mw & 3, cg = mw >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
     const int row = 32 * qd + lane;
     const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
     const int D1w = p.G1 * p.N1;
-    uint32_t it = 0, n_y = 0;
+    const int64_t stride = p.nvox;
+    // stage-3 buffers inside the A2 region: every MID warp must be done reading the last D3 before any
+    // warp overwrites A2 with the next tile
+    const bool s3_in_a2 = p.colA3 < p.colA2 + (uint32_t)(PARTS * D1w / 2) && p.colD3 + p.N3 > p.colA2;
+    uint32_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
-      mbar_wait(&bars.d1_full, it & 1);
+      if (mw == 0) DL_PROF(1, 0);
+      if (it > 0 && s3_in_a2) named_sync(1, kMID * 32);
+      mbar_wait_warp(&bars.d1_full, it & 1);
+      if (mw == 0) DL_PROF(1, 1);
       fence_after();
       for (int ck = cg; ck < D1w / 16; ck += 2) {
         float vv[16];
@@ -307,9 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
       fence_before();
       warp_arrive(&bars.ac_full);
       if (p.free_at == 0) warp_arrive(&bars.d1_free);
-      mbar_wait(&bars.u_full, it & 1);
+      if (mw == 0) DL_PROF(1, 2);
+      mbar_wait_warp(&bars.u_full, it & 1);
+      if (mw == 0) DL_PROF(1, 3);
       fence_after();
       for (int o = 0; o < p.G2; ++o) {
+        // A3 of group o (the MMA finished reading A3 of group o-1: this warp waited y_full below)
         for (int ck = cg; ck < p.N2 / 16; ck += 2) {
           float vv[16];
           ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + ck * 16), vv);
@@ -319,26 +414,39 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
         }
         tmem_wait_st();
         fence_before();
-        warp_arrive(&bars.au_full);
+        warp_arrive(&bars.au_full);   // also: this warp has drained D3 of group o-1
         if (p.free_at == 1 && o == p.G2 - 1) warp_arrive(&bars.d1_free);   // D2 (aliasing D1) fully read
-        mbar_wait(&bars.y_full, n_y & 1);
-        ++n_y;
+        if (mw == 0) DL_PROF(1, 4 + 3 * o);
+        mbar_wait_warp(&bars.y_full, (it * p.G2 + o) & 1);
+        if (mw == 0) DL_PROF(1, 5 + 3 * o);
         fence_after();
-        float* dst = p.out + b * p.out_bs + (int64_t)o * p.C3 * p.nvox + v;
         for (int ck = cg; ck < p.N3 / 16; ck += 2) {
           float vv[16];
           ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
           if (vok) {
+            float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            const int nval = p.C3 - ck * 16;
+            if (nval >= 16) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (ck * 16 + i < p.C3) __stcs(dst + (int64_t)(ck * 16 + i) * p.nvox, vv[i]);
+              for (int i = 0; i < 16; ++i) {
+                __stcs(d, vv[i]);
+                d += stride;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (i < nval) __stcs(d, vv[i]);
+                d += stride;
+              }
+            }
           }
         }
-        fence_before();
+        if (mw == 0) DL_PROF(1, 6 + 3 * o);
       }
-      if (p.free_at == 2) warp_arrive(&bars.d1_free);   // stage-3 buffers (in D1) fully read
+      fence_before();
+      if (p.free_at == 2) warp_arrive(&bars.d1_free);   // stage-3 buffers (inside D1) fully read
     }
-  } else {
+  } else if (warp == kWarpMMA) {
     // =========================== MMA issuer (converged warp, one elected lane issues) ===========
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2), sw3 = smem_u32(smem + p.sm_w3);
     const int km = p.adjoint ? 0 : 1;   // forward: K-major weights; adjoint: MN-major
@@ -349,33 +457,41 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
     const uint32_t id3 = idesc_bf16(128, p.N3, 0, 1 - km);
     const int c1 = km ? p.K1 : p.N1, c2 = km ? K2 : NT2, c3 = km ? p.N2 : p.N3;
     const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(c2, km), ks3 = wkstep(c3, km);
-    uint32_t seq = 0, n_au = 0;
-    auto s1g = [&](uint32_t it, int g) {
-      if (g == 0 && it > 0) {
-        mbar_wait(&bars.d1_free, (it - 1) & 1);
-        fence_after();
-      }
+    uint32_t aslot = 0, around = 0, n_au = 0;
+    // one stage-1 K-step (chunk k of group g); the caller made sure its A slot is full
+    auto s1_chunk = [&](int g, int k) {
       const int wg = p.w1_groups > 1 ? g : 0;
       uint64_t bd[PARTS];
 #pragma unroll
-      for (int j = 0; j < PARTS; ++j) bd[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img, c1, km, 0);
-      const uint32_t d = tbase + p.colD1 + (uint32_t)(g * p.N1);
-      for (int k = 0; k < nk1; ++k, ++seq) {
-        const uint32_t a = seq % p.NA;
-        mbar_wait(&bars.a_full[a], (seq / p.NA) & 1);
-        fence_after();
-        if (elect_one()) {
-          kstep_ts<PARTS>(d, tbase + p.colA + a * kSlotW, 8, bd, id1, k == 0);
-          commit(&bars.a_empty[a]);
-          if (k == nk1 - 1 && g == p.G1 - 1) commit(&bars.d1_full);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd[j] += ks1;
+      for (int j = 0; j < PARTS; ++j)
+        bd[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups + wg) * p.w1_img, c1, km, 0) + (uint64_t)k * ks1;
+      fence_after();
+      if (elect_one()) {
+        kstep_ts<PARTS>(tbase + p.colD1 + (uint32_t)(g * p.N1), tbase + p.colA + aslot * kSlotW, 8, bd, id1, k == 0);
+        commit(&bars.a_empty[aslot]);
+        if (k == nk1 - 1 && g == p.G1 - 1) commit(&bars.d1_full);
+      }
+      __syncwarp();
+      if (++aslot == (uint32_t)p.NA) {
+        aslot = 0;
+        ++around;
       }
     };
+    auto s1_all = [&](uint32_t it) {   // blocking stage 1 of tile it
+      if (it > 0) {
+        mbar_wait_warp(&bars.d1_free, (it - 1) & 1);
+        fence_after();
+      }
+      for (int g = 0; g < p.G1; ++g)
+        for (int k = 0; k < nk1; ++k) {
+          mbar_wait_warp(&bars.a_full[aslot], around & 1);
+          s1_chunk(g, k);
+        }
+    };
     auto s2 = [&](uint32_t it) {
-      mbar_wait(&bars.ac_full, it & 1);
+      DL_PROF(2, 8);
+      mbar_wait_warp(&bars.ac_full, it & 1);
+      DL_PROF(2, 9);
       fence_after();
       for (int o = 0; o < (merge2 ? 1 : p.G2); ++o) {
         uint64_t bd[PARTS];
@@ -392,13 +508,14 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
       if (elect_one()) commit(&bars.u_full);
       __syncwarp();
     };
-    auto s3o = [&](int o) {
+    // stage 3 of group o; the caller made sure its A operand is ready (au_full, which also means D3 is drained)
+    auto s3_issue = [&](uint32_t it, int o) {
+      DL_PROF(2, 11 + 2 * o);
+      ++n_au;
       const int wg = p.w3_groups > 1 ? o : 0;
       uint64_t bd[PARTS];
 #pragma unroll
       for (int j = 0; j < PARTS; ++j) bd[j] = wdesc(sw3 + (uint32_t)(j * p.w3_groups + wg) * p.w3_img, c3, km, 0);
-      mbar_wait(&bars.au_full, n_au & 1);
-      ++n_au;
       fence_after();
       for (int kk = 0; kk < p.N2 / 16; ++kk) {
         if (elect_one()) kstep_ts<PARTS>(tbase + p.colD3, tbase + p.colA3 + 8u * kk, p.N2 / 2, bd, id3, kk == 0);
@@ -411,34 +528,56 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const Chain3 p) {
     };
     const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
     if (p.overlap) {
-      // stage 1 of tile i+1 interleaved with stage 3 of tile i (their TMEM regions are disjoint)
+      // stage 3 of tile i and stage 1 of tile i+1 use disjoint TMEM: issue whichever is ready first
       if (nmine > 0) {
-        for (int g = 0; g < p.G1; ++g) s1g(0, g);
+        s1_all(0);
         s2(0);
       }
-      const int gmax = p.G1 > p.G2 ? p.G1 : p.G2;
       for (uint32_t it = 0; it < nmine; ++it) {
-        for (int o = 0; o < gmax; ++o) {
-          if (it + 1 < nmine && o < p.G1) s1g(it + 1, o);
-          if (o < p.G2) s3o(o);
+        const bool next = it + 1 < nmine;
+        int g1 = 0, k1 = 0, o3 = 0;
+        bool d1ok = !next;   // the next tile's D1 is free once MID has drained this tile's D1
+        bool s1_done = !next;
+        while (!s1_done || o3 < p.G2) {
+          if (o3 < p.G2 && mbar_test(&bars.au_full, n_au & 1)) {
+            s3_issue(it, o3++);
+            continue;
+          }
+          if (!s1_done) {
+            if (!d1ok) d1ok = mbar_test(&bars.d1_free, it & 1);
+            if (d1ok && mbar_test(&bars.a_full[aslot], around & 1)) {
+              s1_chunk(g1, k1);
+              if (++k1 == nk1) {
+                k1 = 0;
+                if (++g1 == p.G1) s1_done = true;
+              }
+            }
+          }
         }
-        if (it + 1 < nmine) s2(it + 1);
+        if (next) s2(it + 1);
       }
     } else {
       for (uint32_t it = 0; it < nmine; ++it) {
-        for (int g = 0; g < p.G1; ++g) s1g(it, g);
+        s1_all(it);
         s2(it);
-        for (int o = 0; o < p.G2; ++o) s3o(o);
+        for (int o = 0; o < p.G2; ++o) {
+          mbar_wait_warp(&bars.au_full, n_au & 1);
+          s3_issue(it, o);
+        }
       }
     }
+  } else if (p.tma) {
+    // =========================== TMA loader ===========================
+    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
   }
   fence_before();
   __syncthreads();
-  if (warp == kWarpLD) tmem_dealloc(tbase, 512);
+  if (warp == kWarpMMA) tmem_dealloc(tbase, 512);
 }
 
 // ============================================================================ LSC weight Gram
 struct GramP {
+  CUtensorMap tm[2];         // channel-pair views of dy (0) and x (1)
   const float* x;
   const float* dy;
   const uint16_t* wM;        // M images (rows RPi, cols NPi), PARTS x groups
@@ -447,23 +586,24 @@ struct GramP {
   float* partials;           // [grid][GR*GC] then db [grid][S_out]
   int64_t nbatch, nvox, x_bs, dy_bs, tiles_per_b;
   int S_in, N, NPi, RPi, S_out, N_out, NPo, RPo, R_out;
-  int wM_groups, base_aligned;
-  int NS, NA;
+  int wM_groups;
+  int NA, ns, tma;
   uint32_t wM_img, wB_img;
-  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_ring, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
+  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_beta, sm_ring, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
   uint32_t colGA, colGB, colGC, colA, colDg, colDc;
   int GR, GC;                // g rows (S_out*RPo), c rows (S_in*RPi)
 };
 
 struct BarsG {
-  uint64_t ld_full[kMaxStages], ld_empty[kMaxStages], a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t dg_full, dg_free, dc_full, dc_free, tiles_full, gram_done;
   float db[4];
   uint32_t tmem_base;
 };
 
-template <int PARTS>
-__global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
+template <int PARTS, int NS>
+__global__ void __launch_bounds__(kThreads, 1) gram_tc(const __grid_constant__ GramP p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -476,16 +616,18 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
     for (uint32_t i = threadIdx.x; i < bB / 16; i += blockDim.x) dB[i] = __ldg(sB + i);
     // operand tiles (and the margin block C over-reads) start zeroed: padding rows stay finite
     uint4* z = reinterpret_cast<uint4*>(smem + p.sm_c);
-    for (uint32_t i = threadIdx.x; i < (p.sm_ring - p.sm_c) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < (p.sm_beta - p.sm_c) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    float* sb = reinterpret_cast<float*>(smem + p.sm_beta);
+    for (int i = threadIdx.x; i < p.RPo; i += blockDim.x) sb[i] = i < p.R_out ? __ldg(p.beta + i) : 0.f;
   }
-  if (warp == kWarpLD) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kWarpMMA) tmem_alloc(&bars.tmem_base, 512);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.NS; ++s) {
-      mbar_init(&bars.ld_full[s], 1);
-      mbar_init(&bars.ld_empty[s], kIN);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], kIN);
     }
     for (int s = 0; s < p.NA; ++s) {
-      mbar_init(&bars.a_full[s], kIN);
+      mbar_init(&bars.a_full[s], 4);   // one arrival per TMEM lane quadrant
       mbar_init(&bars.a_empty[s], 1);
     }
     mbar_init(&bars.dg_full, 1);
@@ -504,52 +646,25 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
   const int nkg = p.NPo / 16, nkc = p.NPi / 16;
-  uint8_t* ring = smem + p.sm_ring;
 
   // chunk sequence per tile: dy groups (S_out x nkg chunks), then x groups (S_in x nkc chunks)
-  if (warp == kWarpLD) {
-    uint32_t seq = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
-      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
-      for (int pass = 0; pass < 2; ++pass) {
-        const int G = pass ? p.S_in : p.S_out, C = pass ? p.N : p.N_out, nk = pass ? nkc : nkg;
-        for (int g = 0; g < G; ++g) {
-          const float* src = (pass ? p.x + b * p.x_bs : p.dy + b * p.dy_bs) + (int64_t)g * C * p.nvox + v0;
-          for (int k = 0; k < nk; ++k, ++seq) {
-            const uint32_t s = seq % p.NS;
-            if (seq >= (uint32_t)p.NS) mbar_wait(&bars.ld_empty[s], ((seq / p.NS) - 1) & 1);
-            load_chunk(ring + s * kChunkBytes, &bars.ld_full[s], src, C, k, p.nvox, safe);
-          }
-        }
-      }
-    }
-  } else if (warp < kIN) {
-    const uint32_t tq = tbase + ((uint32_t)(32 * warp) << 16);
-    const int row = 32 * warp + lane;
-    uint32_t seq = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kTileV;
-      const bool safe = tile_safe(b, v0, p.nvox, p.base_aligned);
-      for (int pass = 0; pass < 2; ++pass) {
-        const int G = pass ? p.S_in : p.S_out, C = pass ? p.N : p.N_out, nk = pass ? nkc : nkg;
-        for (int g = 0; g < G; ++g) {
-          const float* src = (pass ? p.x + b * p.x_bs : p.dy + b * p.dy_bs) + (int64_t)g * C * p.nvox + v0;
-          for (int k = 0; k < nk; ++k, ++seq) {
-            const uint32_t s = seq % p.NS, a = seq % p.NA;
-            mbar_wait(&bars.ld_full[s], (seq / p.NS) & 1);
-            float v[16];
-            read_chunk(ring + s * kChunkBytes, src, C, k, p.nvox, v0, row, safe, v);
-            warp_arrive(&bars.ld_empty[s]);
-            if (seq >= (uint32_t)p.NA) mbar_wait(&bars.a_empty[a], ((seq / p.NA) - 1) & 1);
-            fence_after();
-            split_store16<PARTS>(tq + p.colA + a * kSlotW, 8, v);
-            tmem_wait_st();
-            fence_before();
-            warp_arrive(&bars.a_full[a]);
-          }
-        }
-      }
+  const int ng = p.S_out * nkg, per_tile = ng + p.S_in * nkc;
+  auto geo = [&](int r) {
+    const bool pass = r >= ng;
+    const int rr = pass ? r - ng : r, nk = pass ? nkc : nkg, g = rr / nk, k = rr - g * nk;
+    const int C = pass ? p.N : p.N_out;
+    return ChunkGeo{pass ? 1 : 0, g * C + 16 * k, C - 16 * k};
+  };
+  if (warp < kIN) {
+    const uint32_t tslots = tbase + ((uint32_t)(32 * warp) << 16) + p.colA;
+    if (p.tma) {
+      in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
+                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty);
+    } else {
+      const float* const base[2] = {p.dy, p.x};
+      const int64_t bs[2] = {p.dy_bs, p.x_bs};
+      in_role_cpasync<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots, p.NA, bars.a_full,
+                                 bars.a_empty, reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
     }
   } else if (warp < kWarpMMA) {
     const int mw = warp - kIN, qd = mw & 3, cg = mw >> 2;
@@ -557,43 +672,56 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
     const int row = 32 * qd + lane;
     const int grow = p.GR < 128 ? 128 : p.GR;
     float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
+    // SWIZZLE_128B offsets of this thread's voxel (K index = row): the K-atom / in-row part is fixed,
+    // the 16-byte chunk is XOR-ed with the row-in-group m = j & 7
+    const uint32_t gk = (uint32_t)(row >> 6) * (uint32_t)(grow >> 3) * 1024u + (uint32_t)(row & 7) * 2u;
+    const uint32_t ck_ = (uint32_t)(row >> 6) * (uint32_t)(p.GC >> 3) * 1024u + (uint32_t)(row & 7) * 2u;
+    uint32_t xo[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xo[m] = (uint32_t)m * 128u + ((uint32_t)(((row & 63) >> 3) ^ m) << 4);
+    const float* sbeta = reinterpret_cast<const float*>(smem + p.sm_beta);
     uint32_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       // ---- g -> two-term SW128 tile (+ beta . g for the bias gradient) ----
-      mbar_wait(&bars.dg_full, it & 1);
-      if (it > 0) mbar_wait(&bars.gram_done, (it - 1) & 1);   // previous Gram finished reading the tiles
+      mbar_wait_warp(&bars.dg_full, it & 1);
+      if (it > 0) mbar_wait_warp(&bars.gram_done, (it - 1) & 1);   // previous Gram finished reading the tiles
       fence_after();
-      for (int ck = cg; ck < p.GR / 16; ck += 2) {
+      for (int ck = cg; ck < p.GR / 16; ck += kMID / 4) {
         float vv[16];
         ld16f(tq + p.colDg + (uint32_t)ck * 16, vv);
+        const int o = (ck * 16) / p.RPo, r0 = ck * 16 - o * p.RPo;   // RPo % 16 == 0: one shell per chunk
+        float sdb = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sdb += sbeta[r0 + i] * vv[i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == o) dbacc[q] += sdb;
+        uint8_t* t0 = smem + p.sm_g + gk + (uint32_t)ck * 2048u;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int j = ck * 16 + i;
-          const int o = j / p.RPo, r = j - o * p.RPo;
-          if (r < p.R_out && o < 4) dbacc[o] += __ldg(p.beta + r) * vv[i];
           const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
           const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
-          const uint32_t off = sw128_off(j, row, grow);
-          *reinterpret_cast<uint16_t*>(smem + p.sm_g + off) = (uint16_t)pk0;
-          *reinterpret_cast<uint16_t*>(smem + p.sm_g + p.gtile + off) = (uint16_t)pk1;
+          const uint32_t off = (uint32_t)(i >> 3) * 1024u + xo[i & 7];
+          *reinterpret_cast<uint16_t*>(t0 + off) = (uint16_t)pk0;
+          *reinterpret_cast<uint16_t*>(t0 + p.gtile + off) = (uint16_t)pk1;
         }
       }
       fence_before();
       warp_arrive(&bars.dg_free);
       // ---- c -> two-term SW128 tile ----
-      mbar_wait(&bars.dc_full, it & 1);
+      mbar_wait_warp(&bars.dc_full, it & 1);
       fence_after();
-      for (int ck = cg; ck < p.GC / 16; ck += 2) {
+      for (int ck = cg; ck < p.GC / 16; ck += kMID / 4) {
         float vv[16];
         ld16f(tq + p.colDc + (uint32_t)ck * 16, vv);
+        uint8_t* t0 = smem + p.sm_c + ck_ + (uint32_t)ck * 2048u;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int j = ck * 16 + i;
           const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
           const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
-          const uint32_t off = sw128_off(j, row, p.GC);
-          *reinterpret_cast<uint16_t*>(smem + p.sm_c + off) = (uint16_t)pk0;
-          *reinterpret_cast<uint16_t*>(smem + p.sm_c + p.ctile + off) = (uint16_t)pk1;
+          const uint32_t off = (uint32_t)(i >> 3) * 1024u + xo[i & 7];
+          *reinterpret_cast<uint16_t*>(t0 + off) = (uint16_t)pk0;
+          *reinterpret_cast<uint16_t*>(t0 + p.ctile + off) = (uint16_t)pk1;
         }
       }
       fence_before();
@@ -601,11 +729,11 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
       fence_proxy_async();
       warp_arrive(&bars.tiles_full);
     }
-    if (it > 0) mbar_wait(&bars.gram_done, (it - 1) & 1);
+    if (it > 0) mbar_wait_warp(&bars.gram_done, (it - 1) & 1);
     fence_after();
     // ---- this CTA's Gram partial: G[j (g row)][i (c row)] ----
     float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
-    for (int ck = cg; ck < p.GC / 16; ck += 2) {       // block A: lane = g row
+    for (int ck = cg; ck < p.GC / 16; ck += kMID / 4) {       // block A: lane = g row
       float vv[16];
       ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
       if (row < p.GR)
@@ -647,11 +775,11 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
     const int grow = p.GR < 128 ? 128 : p.GR;
     const uint32_t ASg = (uint32_t)(grow / 8) * 1024u, ASc = (uint32_t)(p.GC / 8) * 1024u;
     const uint64_t ksg = wkstep(p.RPo, 0), ksc = wkstep(p.NPi, 1);
-    uint32_t seq = 0, it = 0;
+    uint32_t aslot = 0, around = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       for (int pass = 0; pass < 2; ++pass) {
         if (it > 0) {
-          mbar_wait(pass ? &bars.dc_free : &bars.dg_free, (it - 1) & 1);
+          mbar_wait_warp(pass ? &bars.dc_free : &bars.dg_free, (it - 1) & 1);
           fence_after();
         }
         const int G = pass ? p.S_in : p.S_out, nk = pass ? nkc : nkg;
@@ -663,23 +791,26 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
             bd[j] = pass ? wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.NPi, 1, 0)
                          : wdesc(sB + (uint32_t)j * p.wB_img, p.RPo, 0, 0);
           const uint32_t d = tbase + (pass ? p.colDc + (uint32_t)(g * p.RPi) : p.colDg + (uint32_t)(g * p.RPo));
-          for (int k = 0; k < nk; ++k, ++seq) {
-            const uint32_t a = seq % p.NA;
-            mbar_wait(&bars.a_full[a], (seq / p.NA) & 1);
+          for (int k = 0; k < nk; ++k) {
+            mbar_wait_warp(&bars.a_full[aslot], around & 1);
             fence_after();
             if (elect_one()) {
-              kstep_ts<PARTS>(d, tbase + p.colA + a * kSlotW, 8, bd, pass ? idc : idg, k == 0);
-              commit(&bars.a_empty[a]);
+              kstep_ts<PARTS>(d, tbase + p.colA + aslot * kSlotW, 8, bd, pass ? idc : idg, k == 0);
+              commit(&bars.a_empty[aslot]);
               if (k == nk - 1 && g == G - 1) commit(pass ? &bars.dc_full : &bars.dg_full);
             }
             __syncwarp();
+            if (++aslot == (uint32_t)p.NA) {
+              aslot = 0;
+              ++around;
+            }
 #pragma unroll
             for (int j = 0; j < PARTS; ++j) bd[j] += pass ? ksc : ksg;
           }
         }
       }
       // ---- Gram over this tile's 128 voxels (two-term split operands, three blocks) ----
-      mbar_wait(&bars.tiles_full, it & 1);
+      mbar_wait_warp(&bars.tiles_full, it & 1);
       fence_after();
       for (int kk = 0; kk < kTileV / 16; ++kk) {
         const uint32_t ko = (uint32_t)(kk >> 2), kb = (uint32_t)(kk & 3) * 32u;
@@ -703,10 +834,12 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const GramP p) {
       if (elect_one()) commit(&bars.gram_done);
       __syncwarp();
     }
+  } else if (p.tma) {
+    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
   }
   fence_before();
   __syncthreads();
-  if (warp == kWarpLD) tmem_dealloc(tbase, 512);
+  if (warp == kWarpMMA) tmem_dealloc(tbase, 512);
 }
 
 // ---------------------------------------------------------------------------- operand packing
@@ -790,6 +923,8 @@ inline int r16(int64_t x) { return (int)((x + 15) / 16 * 16); }
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr int kMaxParts = 256;
+
+long long* g_prof = nullptr;   // debug: phase timestamps of the next chain3 forward launch
 
 int split_terms() {
   static int v = [] {
@@ -894,15 +1029,16 @@ bool plan_chain3(Chain3& p, int parts) {
   p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
   p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
   p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
-  p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 16);
-  const size_t fixed = o + al(sizeof(Bars3), 16);
-  if (fixed + 2 * kChunkBytes > kSmemMax) return false;
-  p.NS = (int)((kSmemMax - fixed) / kChunkBytes);
-  if (p.NS > kMaxStages) p.NS = kMaxStages;
-  p.sm_ring = (uint32_t)o; o = al(o + (size_t)p.NS * kChunkBytes, 16);
-  p.sm_bar = (uint32_t)o; o = al(o + sizeof(Bars3), 16);
-  p.smem_bytes = (uint32_t)o;
-  return o <= kSmemMax;
+  p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 128);
+  p.sm_ring = (uint32_t)o;   // TMA destinations: 128-byte aligned
+  for (p.ns = 8; p.ns >= 2; p.ns /= 2) {   // cp.async ring depth per IN warp
+    size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
+    p.sm_bar = (uint32_t)q;
+    q = al(q + sizeof(Bars3), 16);
+    p.smem_bytes = (uint32_t)q;
+    if (q <= kSmemMax) return true;
+  }
+  return false;
 }
 
 bool plan_gram(GramP& p, int parts) {
@@ -928,21 +1064,23 @@ bool plan_gram(GramP& p, int parts) {
   p.sm_wM = (uint32_t)o; o = al(o + (size_t)parts * p.wM_groups * p.wM_img, 1024);
   p.sm_wB = (uint32_t)o; o = al(o + (size_t)parts * p.wB_img, 1024);
   p.sm_c = (uint32_t)o; o = al(o + (size_t)2 * p.ctile, 1024);
+  // block C reads c rows up to 191 of every K-atom: they land in the g tile that follows c
   p.sm_g = (uint32_t)o; o = al(o + (size_t)2 * p.gtile, 1024);
-  o = al(o + 8192, 1024);   // block C reads c rows up to 191 of every K-atom: keep mapped smem after g
-  const size_t fixed = o + al(sizeof(BarsG), 16);
-  if (fixed + 2 * kChunkBytes > kSmemMax) return false;
-  p.NS = (int)((kSmemMax - fixed) / kChunkBytes);
-  if (p.NS > kMaxStages) p.NS = kMaxStages;
-  p.sm_ring = (uint32_t)o; o = al(o + (size_t)p.NS * kChunkBytes, 16);
-  p.sm_bar = (uint32_t)o; o = al(o + sizeof(BarsG), 16);
-  p.smem_bytes = (uint32_t)o;
-  return o <= kSmemMax;
+  p.sm_beta = (uint32_t)o; o = al(o + (size_t)p.RPo * 4, 128);
+  p.sm_ring = (uint32_t)o;
+  for (p.ns = 8; p.ns >= 2; p.ns /= 2) {
+    size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
+    p.sm_bar = (uint32_t)q;
+    q = al(q + sizeof(BarsG), 16);
+    p.smem_bytes = (uint32_t)q;
+    if (q <= kSmemMax) return true;
+  }
+  return false;
 }
 
 template <int PARTS>
 int run_chain3(const Chain3& p, int grid, cudaStream_t st) {
-  auto k = chain3_tc<PARTS>;
+  auto k = p.ns == 8 ? chain3_tc<PARTS, 8> : p.ns == 4 ? chain3_tc<PARTS, 4> : chain3_tc<PARTS, 2>;
   DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
   k<<<grid, kThreads, p.smem_bytes, st>>>(p);
   return after_launch("chain3_tc");
@@ -950,7 +1088,7 @@ int run_chain3(const Chain3& p, int grid, cudaStream_t st) {
 
 template <int PARTS>
 int run_gram(const GramP& p, int grid, cudaStream_t st) {
-  auto k = gram_tc<PARTS>;
+  auto k = p.ns == 8 ? gram_tc<PARTS, 8> : p.ns == 4 ? gram_tc<PARTS, 4> : gram_tc<PARTS, 2>;
   DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
   k<<<grid, kThreads, p.smem_bytes, st>>>(p);
   return after_launch("gram_tc");
@@ -1025,15 +1163,49 @@ bool chain_fits(const Dims& d) {
   return plan_chain3(f, d.parts) && plan_chain3(a, d.parts) && plan_gram(g, d.parts);
 }
 
+// Channel-pair view of a (nbatch, rows, nvox) fp32 tensor for TMA: element (u, j, b) is channel 2j + u / nvox,
+// voxel u % nvox -- rows 2j and 2j+1 are contiguous, so the row stride 8*nvox bytes is 16-byte aligned for
+// any even nvox.  Box = 132 voxels x 8 channel pairs.  False (use the cp.async path) if not expressible.
+bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, int64_t group_rows, int64_t nvox) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      fn = nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode || !base || nvox % 2 || rows % 2 || group_rows % 2 || ((uintptr_t)base & 15) ||
+      2 * nvox + kTileV >= ((int64_t)1 << 31) || nbatch >= ((int64_t)1 << 31) || rows / 2 > ((int64_t)1 << 31))
+    return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * nvox), (cuuint64_t)(rows / 2), (cuuint64_t)nbatch};
+  const cuuint64_t strides[2] = {(cuuint64_t)(8 * nvox), (cuuint64_t)(4 * rows * nvox)};
+  const cuuint32_t box[3] = {(cuuint32_t)kBoxV, 8u, 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_disabled() {
+  static const bool v = getenv("DELIMIT_NO_TMA") != nullptr;
+  return v;
+}
+
 int grid_for(int64_t ntiles, int sm) { return (int)(ntiles < sm ? (ntiles > 0 ? ntiles : 1) : sm); }
 
-int aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0 ? 1 : 0; }
 
 }  // namespace
 }  // namespace tc
 }  // namespace dl
 
 extern "C" {
+
+// Debug hook (not part of the documented ABI): record chain3 phase timestamps of CTA 0 into
+// `buf` (device, >= 8*4*32 int64) on subsequent forward launches; NULL disables.
+void dl_debug_chain_prof(void* buf) { dl::tc::g_prof = reinterpret_cast<long long*>(buf); }
 
 int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
                        int m_per_shell) {
@@ -1070,7 +1242,8 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   p.in = x;
   p.out = y;
   p.bias2 = bvec;
-  p.base_aligned = aligned16(x);
+  p.prof = g_prof;
+  p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
   return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
 }
@@ -1098,7 +1271,7 @@ int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, floa
     p.in = dy;
     p.out = dx;
     p.bias2 = nullptr;
-    p.base_aligned = aligned16(dy);
+    p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
     const int grid = grid_for(ntiles, sm);
     DL_TRY(d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st));
   }
@@ -1111,7 +1284,8 @@ int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, floa
       g.x = x;
       g.dy = dy;
       g.beta = beta;
-      g.base_aligned = aligned16(x) && aligned16(dy);
+      g.tma = !tma_disabled() && pair_map(&g.tm[0], dy, nbatch, s_out * n_out, n_out, nvox) &&
+              pair_map(&g.tm[1], x, nbatch, s_in * n, n, nvox);
       nparts = grid_for(ntiles, sm < kMaxParts ? sm : kMaxParts);
       DL_TRY(d.parts == 3 ? run_gram<3>(g, nparts, st) : run_gram<2>(g, nparts, st));
     }

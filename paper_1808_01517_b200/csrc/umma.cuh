@@ -178,6 +178,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// mbar_wait by a whole warp, reconverged afterwards (lanes leave the polling loop independently, and
+// the .sync.aligned tcgen05 ops / elect.sync that follow need the full warp).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+  __syncwarp();
+}
+
 // Arrive once and add `tx` expected transaction bytes to the current phase.
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t tx) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(
@@ -193,6 +200,41 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// Tiled 3-D tensor copy global -> shared through a CUtensorMap (TMA); out-of-range elements are
+// zero-filled and still counted, so every copy completes the full box size as tx bytes on `bar`.
+// `tmap` is the generic address of a __grid_constant__ kernel parameter.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 4-byte asynchronous global -> shared copy (LDGSTS); src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Non-blocking: true if the phase with `parity` has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 // Named barrier over `count` threads (id 1..15; 0 is __syncthreads).
@@ -220,8 +262,10 @@ __device__ __forceinline__ void split_pair(float a, float b, uint32_t (&part)[NP
   for (int i = 0; i < NP; ++i) {
     const uint32_t p = pack_bf16x2(a, b);
     part[i] = p;
-    a -= bf16lo_to_f32(p);
-    b -= bf16hi_to_f32(p);
+    if (i + 1 < NP) {   // the last residual is never used
+      a -= bf16lo_to_f32(p);
+      b -= bf16hi_to_f32(p);
+    }
   }
 }
 
