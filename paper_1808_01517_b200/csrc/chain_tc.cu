@@ -137,18 +137,19 @@ __device__ __forceinline__ void stream_chunk(float* dst, const float* src, int64
 }
 
 // Hands one voxel's 16 values (split into PARTS bf16 terms) to the MMA warp through TMEM A slot
-// (aslot, around); advances the slot cursor.
+// (aslot, around), then advances the slot cursor by `step` chunks.
 template <int PARTS>
 __device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int NA, uint64_t* a_full,
-                                      uint64_t* a_empty, uint32_t& aslot, uint32_t& around) {
+                                      uint64_t* a_empty, uint32_t& aslot, uint32_t& around, int step = 1) {
   if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
   fence_after();
   split_store16<PARTS>(tslots + aslot * (PARTS * 8), 8, v);
   tmem_wait_st();
   fence_before();
   warp_arrive(&a_full[aslot]);
-  if (++aslot == (uint32_t)NA) {
-    aslot = 0;
+  aslot += step;
+  while (aslot >= (uint32_t)NA) {
+    aslot -= NA;
     ++around;
   }
 }
@@ -159,19 +160,19 @@ struct ChunkGeo {
   int tensor, c0, nval;
 };
 
-// Fallback IN role (no tensor map): each warp streams its own 32-voxel segment of every chunk through
-// a private NS-deep ring with 4-byte cp.async (any alignment).  Every thread only reads back what it
-// copied itself, so cp.async.wait_group is the only synchronisation.
+// Fallback IN role (no tensor map): each warp streams its own 32-voxel segment of its chunks
+// q = iw, iw + nIW, ... through a private NS-deep ring with 4-byte cp.async (any alignment).  Every
+// thread only reads back what it copied itself, so cp.async.wait_group is the only synchronisation.
 template <int PARTS, int NS, typename Geo>
 __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                                 int64_t nvox, const float* const (&base)[2], const int64_t (&bs)[2],
                                                 uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
-                                                float* ring) {
+                                                float* ring, int iw = 0, int nIW = 1) {
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int64_t nmine = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = nmine * per_tile;
-  int64_t qp = 0;
-  uint32_t pslot = 0, cslot = 0, aslot = 0, around = 0;
+  int64_t qp = iw;
+  uint32_t pslot = 0, cslot = 0, aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
   auto issue = [&]() {
     if (qp < total) {
       const int64_t ti = qp / per_tile;
@@ -182,14 +183,14 @@ __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, in
       const bool vok = v < nvox;
       const float* src = base[cg.tensor] + b * bs[cg.tensor] + (int64_t)cg.c0 * nvox + (vok ? v : 0);
       stream_chunk(ring + pslot * 512 + lane, src, nvox, vok ? cg.nval : 0, base[0]);
-      ++qp;
+      qp += nIW;
     }
     cp_async_commit();
     pslot = pslot + 1 == NS ? 0 : pslot + 1;
   };
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) issue();
-  for (int64_t q = 0; q < total; ++q) {
+  for (int64_t q = iw; q < total; q += nIW) {
     issue();
     cp_async_wait<NS - 1>();
     float v[16];
@@ -197,7 +198,7 @@ __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, in
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = rp[r * 32];
     cslot = cslot + 1 == NS ? 0 : cslot + 1;
-    put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around);
+    put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
   }
   cp_async_wait<0>();
 }
@@ -239,31 +240,55 @@ __device__ __forceinline__ void tma_loader(const Geo& geo, int per_tile, int64_t
 }
 
 // IN role over the TMA ring: thread = voxel; row j of the chunk is channel-pair row j/2 of box j%2.
+// This warp takes chunks q = iw, iw + nIW, ... (nIW a power of two).
 template <int PARTS, int NS, typename Geo>
 __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                             int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
-                                            const float* ring, uint64_t* full, uint64_t* empty) {
+                                            const float* ring, uint64_t* full, uint64_t* empty, int iw = 0,
+                                            int nIW = 1, long long* prof = nullptr) {
+  long long tw_full = 0, tw_empty = 0, tw_split = 0, n_ch = 0;
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int odd0 = 8 * kBoxV + (int)(nvox & 3);   // first odd-channel value of this thread, minus its voxel
-  uint32_t s = 0, round = 0, aslot = 0, around = 0;
+  uint32_t s = 0, round = 0, aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
+  uint32_t q = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t b = t / tiles_per_b;
     const bool vok = (t - b * tiles_per_b) * kTileV + 32 * qd + lane < nvox;
-    for (int r = 0; r < per_tile; ++r) {
-      const ChunkGeo cg = geo(r);
-      const int nval = vok ? cg.nval : 0;   // the odd-channel box reads past nvox into the next row
-      mbar_wait_warp(&full[s], round & 1);
-      const float* rp = ring + s * (kStageBytes / 4) + 32 * qd + lane;
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = j < nval ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
-      warp_arrive(&empty[s]);
+    for (int r = 0; r < per_tile; ++r, ++q) {
+      const uint32_t cs = s;
+      const uint32_t cround = round;
       if (++s == NS) {
         s = 0;
         ++round;
       }
-      put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around);
+      if ((q & (uint32_t)(nIW - 1)) != (uint32_t)iw) continue;
+      const ChunkGeo cg = geo(r);
+      const int nval = vok ? cg.nval : 0;   // voxels past nvox read neighbouring-row data: zero them
+      long long c0 = clock64();
+      mbar_wait_warp(&full[cs], cround & 1);
+      long long c1 = clock64();
+      const float* rp = ring + cs * (kStageBytes / 4) + 32 * qd + lane;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = j < nval ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+      warp_arrive(&empty[cs]);
+      long long c2 = clock64();
+      if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
+      long long c3 = clock64();
+      put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
+      long long c4 = clock64();
+      tw_full += c1 - c0;
+      tw_empty += c3 - c2;
+      tw_split += c4 - c3 + c2 - c1;
+      ++n_ch;
     }
+  }
+  if (prof && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    prof[1024 + 4 * w + 0] = n_ch;
+    prof[1024 + 4 * w + 1] = tw_full;
+    prof[1024 + 4 * w + 2] = tw_empty;
+    prof[1024 + 4 * w + 3] = tw_split;
   }
 }
 
@@ -283,6 +308,8 @@ struct Chain3 {
   int w1_groups, w3_groups;
   int adjoint, overlap, free_at, tma;
   int NA, ns;                         // TMEM A slots, ring depth
+  int NAc;                            // chain3v: conversion-ring slots
+  uint32_t colC;                      // chain3v: conversion ring (A operands of stages 2 and 3)
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
   uint32_t colA, colD1, colA2, colD2, colA3, colD3;
@@ -573,6 +600,298 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
   fence_before();
   __syncthreads();
   if (warp == kWarpMMA) tmem_dealloc(tbase, 512);
+}
+
+// ============================================================================ chain3v kernel
+// Same three stages, but every accumulator stays resident (D1 | D2 | D3) and the A operands of all
+// stages stream through two small TMEM rings, so the MMA warp can interleave the next tile's stage 1
+// with this tile's stages 2/3 whenever a D3 drain or a conversion is in flight:
+//   warps 0-7    IN   (two per lane quadrant, alternate chunks) -> IN ring (colA, NA slots)
+//   warps 8-15   CONV D1 chunks -> conversion ring (colC, NAc slots) for stage 2, then D2 (+bias)
+//                chunks for stage 3 of every output group (two per quadrant, alternate items)
+//   warps 16-23  OUT  D3 -> HBM (two per quadrant, alternate 16-column chunks)
+//   warp 24      MMA, warp 25 TMA loader.
+// Ordering facts that replace explicit "free" barriers: CONV reads D1(t) only in the stage-2 items of
+// tile t and D2(t-1) only before the first stage-2 item of tile t, so the MMA may overwrite D1 once it
+// has consumed stage-2 item nk2-1 of tile t, and D2 once it consumes stage-2 item 0 of tile t+1.
+constexpr int kIN3 = 8, kCV3 = 8, kOUT3 = 8;
+constexpr int kW3MMA = kIN3 + kCV3 + kOUT3;   // 24
+constexpr int kW3LD = kW3MMA + 1;             // 25
+constexpr int kThreads3 = (kW3LD + 1) * 32;
+
+struct Bars3v {
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];
+  uint64_t d1_full, d2_full, d3_full, d3_free;
+  uint32_t tmem_base;
+};
+
+template <int PARTS, int NS>
+__global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant__ Chain3 p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  Bars3v& bars = *reinterpret_cast<Bars3v*>(smem + p.sm_bar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kSlotW = PARTS * 8;
+
+  {  // stage weight images + bias once per CTA
+    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = (uint32_t)PARTS * p.w2_img,
+                   b3 = (uint32_t)PARTS * p.w3_groups * p.w3_img;
+    const uint4 *s1 = reinterpret_cast<const uint4*>(p.w1), *s2 = reinterpret_cast<const uint4*>(p.w2),
+                *s3 = reinterpret_cast<const uint4*>(p.w3);
+    uint4 *d1 = reinterpret_cast<uint4*>(smem + p.sm_w1), *d2 = reinterpret_cast<uint4*>(smem + p.sm_w2),
+          *d3 = reinterpret_cast<uint4*>(smem + p.sm_w3);
+    for (uint32_t i = threadIdx.x; i < b1 / 16; i += blockDim.x) d1[i] = __ldg(s1 + i);
+    for (uint32_t i = threadIdx.x; i < b2 / 16; i += blockDim.x) d2[i] = __ldg(s2 + i);
+    for (uint32_t i = threadIdx.x; i < b3 / 16; i += blockDim.x) d3[i] = __ldg(s3 + i);
+    float* sb = reinterpret_cast<float*>(smem + p.sm_bias);
+    for (int i = threadIdx.x; i < p.G2 * p.N2; i += blockDim.x) {
+      const int o = i / p.N2, r = i - o * p.N2;
+      sb[i] = (p.bias2 && r < p.C2) ? __ldg(p.bias2 + o * p.C2 + r) : 0.f;
+    }
+  }
+  if (warp == kW3MMA) tmem_alloc(&bars.tmem_base, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 4);
+    }
+    for (int s = 0; s < p.NA; ++s) {
+      mbar_init(&bars.a_full[s], 4);
+      mbar_init(&bars.a_empty[s], 1);
+    }
+    for (int s = 0; s < p.NAc; ++s) {
+      mbar_init(&bars.c_full[s], 4);   // one CONV warp per quadrant converts each item
+      mbar_init(&bars.c_empty[s], 1);
+    }
+    mbar_init(&bars.d1_full, 1);
+    mbar_init(&bars.d2_full, 1);
+    mbar_init(&bars.d3_full, 1);
+    mbar_init(&bars.d3_free, kOUT3);
+    mbar_fence_init();
+  }
+  fence_proxy_async();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = bars.tmem_base;
+  const int64_t ntiles = p.nbatch * p.tiles_per_b;
+  const int nk1 = p.K1 / 16, per_tile = p.G1 * nk1;
+  const int K2 = p.G1 * p.N1, nk2 = K2 / 16, nk3 = p.N2 / 16;
+  auto geo = [&](int r) {
+    const int g = r / nk1, k = r - g * nk1;
+    return ChunkGeo{0, g * p.C1 + 16 * k, p.C1 - 16 * k};
+  };
+
+  if (warp < kIN3) {
+    // =========================== IN ===========================
+    const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
+    if (p.tma) {
+      in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
+                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty, warp >> 2, 2,
+                             p.prof);
+    } else if (warp < 4) {
+      const float* const base[2] = {p.in, p.in};
+      const int64_t bs[2] = {p.in_bs, p.in_bs};
+      in_role_cpasync<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots, p.NA, bars.a_full,
+                                 bars.a_empty, reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
+    }
+  } else if (warp < kIN3 + kCV3) {
+    // =========================== CONV: accumulators -> conversion ring ===========================
+    // items per tile: nk2 D1 chunks (stage-2 A), then G2 x nk3 D2 chunks (+bias, stage-3 A); this warp
+    // converts items i = cw, cw + 2, ... of the CTA-wide sequence (slot i % NAc)
+    const int cw = (warp - kIN3) >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
+    const int per_c = nk2 + p.G2 * nk3;
+    uint32_t cslot = (uint32_t)(cw % p.NAc), cround = (uint32_t)(cw / p.NAc), it = 0;
+    int i0 = cw;   // first item of this warp in the current tile
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      if (warp == kIN3) DL_PROF(1, 0);
+      mbar_wait_warp(&bars.d1_full, it & 1);
+      if (warp == kIN3) DL_PROF(1, 1);
+      fence_after();
+      bool d2_seen = false;
+      int i = i0;
+      for (; i < per_c; i += 2) {
+        float v[16];
+        if (i < nk2) {
+          ld16f(tq + p.colD1 + (uint32_t)i * 16, v);
+        } else {
+          if (!d2_seen) {
+            if (warp == kIN3) DL_PROF(1, 2);
+            mbar_wait_warp(&bars.d2_full, it & 1);
+            if (warp == kIN3) DL_PROF(1, 3);
+            fence_after();
+            d2_seen = true;
+          }
+          const int o = (i - nk2) / nk3, j = (i - nk2) - o * nk3;
+          ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + 16 * j), v);
+          const float* bb = sb + o * p.N2 + 16 * j;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] += bb[e];
+        }
+        if (cround > 0) mbar_wait_warp(&bars.c_empty[cslot], (cround - 1) & 1);
+        fence_after();
+        split_store16<PARTS>(tq + p.colC + cslot * kSlotW, 8, v);
+        tmem_wait_st();
+        fence_before();
+        warp_arrive(&bars.c_full[cslot]);
+        cslot += 2;
+        while (cslot >= (uint32_t)p.NAc) {
+          cslot -= p.NAc;
+          ++cround;
+        }
+      }
+      i0 = i - per_c;   // items carry over tile boundaries when per_c is odd
+    }
+  } else if (warp < kW3MMA) {
+    // =========================== OUT: D3 -> HBM ===========================
+    const int ow = warp - kIN3 - kCV3, qd = warp & 3, cg = ow >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
+    const int row = 32 * qd + lane;
+    const int64_t stride = p.nvox;
+    uint32_t n3 = 0, it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
+      const bool vok = v < p.nvox;
+      for (int o = 0; o < p.G2; ++o, ++n3) {
+        mbar_wait_warp(&bars.d3_full, n3 & 1);
+        if (ow == 0) DL_PROF(1, 8 + 2 * o);
+        fence_after();
+        for (int ck = cg; ck < p.N3 / 16; ck += 2) {
+          float vv[16];
+          ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
+          if (vok) {
+            float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            const int nval = p.C3 - ck * 16;
+            if (nval >= 16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                __stcs(d, vv[i]);
+                d += stride;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (i < nval) __stcs(d, vv[i]);
+                d += stride;
+              }
+            }
+          }
+        }
+        fence_before();
+        warp_arrive(&bars.d3_free);
+        if (ow == 0) DL_PROF(1, 9 + 2 * o);
+      }
+    }
+  } else if (warp == kW3MMA) {
+    // =========================== MMA issuer ===========================
+    // Lean loop: descriptors advance by additions; stage/group cursors are incremental.
+    const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2), sw3 = smem_u32(smem + p.sm_w3);
+    const int km = p.adjoint ? 0 : 1;
+    const int NT2 = p.G2 * p.N2;
+    const int n2m = NT2 <= 256 ? 1 : p.G2;   // stage-2 MMAs per item (N split when > 256)
+    const uint32_t id1 = idesc_bf16(128, p.N1, 0, 1 - km);
+    const uint32_t id2 = idesc_bf16(128, n2m == 1 ? NT2 : p.N2, 0, 1 - km);
+    const uint32_t id3 = idesc_bf16(128, p.N3, 0, 1 - km);
+    const int c1 = km ? p.K1 : p.N1, c2 = km ? K2 : NT2, c3 = km ? p.N2 : p.N3;
+    const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(c2, km), ks3 = wkstep(c3, km);
+    uint64_t B1[PARTS], B2[PARTS], B3[PARTS];
+#pragma unroll
+    for (int j = 0; j < PARTS; ++j) {
+      B1[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups) * p.w1_img, c1, km, 0);
+      B2[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, c2, km, 0);
+      B3[j] = wdesc(sw3 + (uint32_t)(j * p.w3_groups) * p.w3_img, c3, km, 0);
+    }
+    const uint64_t g1s = p.w1_groups > 1 ? (uint64_t)(p.w1_img >> 4) : 0;   // next group's image
+    const uint64_t g3s = p.w3_groups > 1 ? (uint64_t)(p.w3_img >> 4) : 0;
+    const uint64_t o2s = wdesc(0, c2, km, p.N2) - wdesc(0, c2, km, 0);      // next N2 block of stage 2
+    const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    const uint32_t tA = tbase + p.colA, tC = tbase + p.colC, tD1 = tbase + p.colD1, tD2 = tbase + p.colD2,
+                   tD3 = tbase + p.colD3;
+    // Static issue order per tile t: stage 2(t); then for each output group o: stage 3(t, o) followed by
+    // a share of stage 1(t+1) -- those MMAs run while OUT drains D3(o).  All waits block (no polling).
+    uint32_t aslot = 0, around = 0, cslot = 0, cround = 0, n3 = 0;
+    auto s1_chunk = [&](int g, int k) {
+      mbar_wait_warp(&bars.a_full[aslot], around & 1);
+      fence_after();
+      uint64_t bd[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s + (uint64_t)k * ks1;
+      if (elect_one()) {
+        kstep_ts<PARTS>(tD1 + (uint32_t)(g * p.N1), tA + aslot * kSlotW, 8, bd, id1, k == 0);
+        commit(&bars.a_empty[aslot]);
+        if (k == nk1 - 1 && g == p.G1 - 1) commit(&bars.d1_full);
+      }
+      __syncwarp();
+      if (++aslot == (uint32_t)p.NA) {
+        aslot = 0;
+        ++around;
+      }
+    };
+    auto c_take = [&]() {   // wait for the next conversion-ring item; returns its A address
+      mbar_wait_warp(&bars.c_full[cslot], cround & 1);
+      fence_after();
+      return tC + cslot * kSlotW;
+    };
+    auto c_release = [&](uint64_t* extra) {
+      if (elect_one()) {
+        commit(&bars.c_empty[cslot]);
+        if (extra) commit(extra);
+      }
+      __syncwarp();
+      if (++cslot == (uint32_t)p.NAc) {
+        cslot = 0;
+        ++cround;
+      }
+    };
+    const int n1 = p.G1 * nk1;
+    for (int q = 0; q < (nmine > 0 ? n1 : 0); ++q) s1_chunk(q / nk1, q % nk1);
+    for (uint32_t it = 0; it < nmine; ++it) {
+      DL_PROF(2, 0);
+      // ---- stage 2 ----
+      for (int jj = 0; jj < nk2; ++jj) {
+        const uint32_t a0 = c_take();
+        uint64_t bd[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd[j] = B2[j] + (uint64_t)jj * ks2;
+        for (int oo = 0; oo < n2m; ++oo) {
+          if (elect_one()) kstep_ts<PARTS>(tD2 + (uint32_t)(oo * p.N2), a0, 8, bd, id2, jj == 0);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] += o2s;
+        }
+        c_release(jj == nk2 - 1 ? &bars.d2_full : nullptr);
+      }
+      DL_PROF(2, 1);
+      // ---- stage 3 per output group, interleaved with the next tile's stage 1 ----
+      const bool next = it + 1 < nmine;
+      int q1 = 0;
+      for (int o = 0; o < p.G2; ++o) {
+        if (n3 > 0) mbar_wait_warp(&bars.d3_free, (n3 - 1) & 1);
+        DL_PROF(2, 2 + 2 * o);
+        for (int jj = 0; jj < nk3; ++jj) {
+          const uint32_t a0 = c_take();
+          uint64_t bd[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] = B3[j] + (uint64_t)o * g3s + (uint64_t)jj * ks3;
+          if (elect_one()) kstep_ts<PARTS>(tD3, a0, 8, bd, id3, jj == 0);
+          __syncwarp();
+          c_release(jj == nk3 - 1 ? &bars.d3_full : nullptr);
+        }
+        ++n3;
+        DL_PROF(2, 3 + 2 * o);
+        if (next)
+          for (const int qe = n1 * (o + 1) / p.G2; q1 < qe; ++q1) s1_chunk(q1 / nk1, q1 % nk1);
+      }
+    }
+  } else if (p.tma) {
+    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kW3MMA) tmem_dealloc(tbase, 512);
 }
 
 // ============================================================================ LSC weight Gram
@@ -1041,6 +1360,43 @@ bool plan_chain3(Chain3& p, int parts) {
   return false;
 }
 
+// chain3v: D1 | D2 | D3 resident, IN ring (NA) + conversion ring (NAc) in the remaining columns.
+bool plan_chain3v(Chain3& p, int parts) {
+  if (p.N1 > 256 || p.N2 > 256 || p.N3 > 256 || p.G1 * p.N1 > 512) return false;
+  const int slotw = parts * 8, D1w = p.G1 * p.N1, D2w = p.G2 * p.N2, D3w = p.N3;
+  const int nslots = (512 - D1w - D2w - D3w) / slotw;
+  if (512 - D1w - D2w - D3w < 0 || nslots < 4) return false;
+  p.NA = nslots / 2 < kMaxSlots ? nslots / 2 : kMaxSlots;
+  p.NAc = nslots - p.NA < kMaxSlots ? nslots - p.NA : kMaxSlots;
+  p.colA = 0;
+  p.colC = (uint32_t)(p.NA * slotw);
+  p.colD1 = p.colC + (uint32_t)(p.NAc * slotw);
+  p.colD2 = p.colD1 + (uint32_t)D1w;
+  p.colD3 = p.colD2 + (uint32_t)D2w;
+  p.w1_img = (uint32_t)(p.N1 * p.K1 * 2);
+  p.w2_img = (uint32_t)((p.G2 * p.N2) * (p.G1 * p.N1) * 2);
+  p.w3_img = (uint32_t)(p.N3 * p.N2 * 2);
+  size_t o = 0;
+  p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
+  p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
+  p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
+  p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 128);
+  p.sm_ring = (uint32_t)o;
+  for (p.ns = kMaxStages; p.ns >= 2; --p.ns) {
+    size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
+    p.sm_bar = (uint32_t)q;
+    q = al(q + sizeof(Bars3v), 16);
+    p.smem_bytes = (uint32_t)q;
+    if (q <= kSmemMax) return true;
+  }
+  return false;
+}
+
+bool use_v3() {
+  static const bool v = getenv("DELIMIT_CHAIN_V2") == nullptr;
+  return v;
+}
+
 bool plan_gram(GramP& p, int parts) {
   p.GR = p.S_out * p.RPo;
   p.GC = p.S_in * p.RPi;
@@ -1084,6 +1440,34 @@ int run_chain3(const Chain3& p, int grid, cudaStream_t st) {
   DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
   k<<<grid, kThreads, p.smem_bytes, st>>>(p);
   return after_launch("chain3_tc");
+}
+
+template <int PARTS, int NS>
+int launch_chain3v(const Chain3& p, int grid, cudaStream_t st) {
+  DL_CUDA(cudaFuncSetAttribute(chain3v_tc<PARTS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+  chain3v_tc<PARTS, NS><<<grid, kThreads3, p.smem_bytes, st>>>(p);
+  return after_launch("chain3v_tc");
+}
+
+template <int PARTS>
+int run_chain3v(const Chain3& p, int grid, cudaStream_t st) {
+  switch (p.ns) {
+    case 2: return launch_chain3v<PARTS, 2>(p, grid, st);
+    case 3: return launch_chain3v<PARTS, 3>(p, grid, st);
+    case 4: return launch_chain3v<PARTS, 4>(p, grid, st);
+    case 5: return launch_chain3v<PARTS, 5>(p, grid, st);
+    case 6: return launch_chain3v<PARTS, 6>(p, grid, st);
+    case 7: return launch_chain3v<PARTS, 7>(p, grid, st);
+    default: return launch_chain3v<PARTS, 8>(p, grid, st);
+  }
+}
+
+// plan + launch one chain3 direction on the best kernel that fits
+int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* what) {
+  Chain3 v = p;
+  if (use_v3() && plan_chain3v(v, d.parts)) return d.parts == 3 ? run_chain3v<3>(v, grid, st) : run_chain3v<2>(v, grid, st);
+  if (!plan_chain3(p, d.parts)) return dl::fail(DL_EINVAL, "%s: channel counts exceed the fused kernel's plan", what);
+  return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
 }
 
 template <int PARTS>
@@ -1160,7 +1544,11 @@ bool chain_fits(const Dims& d) {
   Chain3 f = chain3_params(d, ws_layout(d, 1), nullptr, false);
   Chain3 a = chain3_params(d, ws_layout(d, 1), nullptr, true);
   GramP g = gram_params(d, ws_layout(d, 1), nullptr);
-  return plan_chain3(f, d.parts) && plan_chain3(a, d.parts) && plan_gram(g, d.parts);
+  auto fits = [&](Chain3 c) {
+    Chain3 v = c;
+    return (use_v3() && plan_chain3v(v, d.parts)) || plan_chain3(c, d.parts);
+  };
+  return fits(f) && fits(a) && plan_gram(g, d.parts);
 }
 
 // Channel-pair view of a (nbatch, rows, nvox) fp32 tensor for TMA: element (u, j, b) is channel 2j + u / nvox,
@@ -1235,7 +1623,7 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   WsLayout w = ws_layout(d, kMaxParts);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   Chain3 p = chain3_params(d, w, ws, false);
-  DL_REQUIRE(plan_chain3(p, d.parts), "chain_fwd: channel counts exceed the fused kernel's TMEM/smem plan");
+  DL_REQUIRE(chain_fits(d), "chain_fwd: channel counts exceed the fused kernel's TMEM/smem plan");
   if (nbatch == 0 || nvox == 0) return DL_OK;
   cudaStream_t st = dl::as_stream(stream);
   DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
@@ -1245,7 +1633,7 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   p.prof = g_prof;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
-  return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
+  return run_chain(p, d, grid, st, "chain_fwd");
 }
 
 int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, float* db, const float* M, int m_per_shell,
@@ -1267,13 +1655,12 @@ int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, floa
   DL_TRY(pack_all(d, w, ws, M, dx ? L : nullptr, Bt, st));
   if (dx && ntiles > 0) {
     Chain3 p = chain3_params(d, w, ws, true);
-    DL_REQUIRE(plan_chain3(p, d.parts), "chain_bwd: channel counts exceed the fused kernel's plan");
     p.in = dy;
     p.out = dx;
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
     const int grid = grid_for(ntiles, sm);
-    DL_TRY(d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st));
+    DL_TRY(run_chain(p, d, grid, st, "chain_bwd"));
   }
   if (dW || db) {
     GramP g = gram_params(d, w, ws);

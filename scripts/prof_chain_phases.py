@@ -1,15 +1,22 @@
-"""Debug: per-role phase timestamps of CTA 0 in the forward chain3 kernel (dl_debug_chain_prof)."""
-import ctypes, sys
-import numpy as np
+"""Debug: per-role phase timestamps of CTA 0 in the forward chain kernel (dl_debug_chain_prof).
+
+Prints, for tiles 2..5, every recorded event (role, event id) as cycles since tile 2's first event.
+chain3v events (role 1): 0 CONV waits d1, 1 d1 ready, 2 D1 converted, 3 d2 ready, 4+o A3(o) converted,
+8+2o OUT sees d3(o), 9+2o OUT drained d3(o).
+"""
+import ctypes
+import sys
+
 import torch
+
 sys.path.insert(0, '/root/repo')
-import bench
-from paper_1808_01517_b200 import _lib
+import bench  # noqa: E402
+from paper_1808_01517_b200 import _lib  # noqa: E402
 
 dev = torch.device('cuda:0')
 dirs, lsc, chain = bench.build_model(dev)
 x, dy = bench.synth_inputs(dirs, (145, 174, 145), 0, dev)
-buf = torch.zeros(2048, dtype=torch.int64, device=dev)
+buf = torch.zeros(4096, dtype=torch.int64, device=dev)
 lib = _lib.load()
 for _ in range(2):
     y = chain(x)
@@ -18,17 +25,13 @@ lib.dl_debug_chain_prof(ctypes.c_void_p(buf.data_ptr()))
 y = chain(x)
 torch.cuda.synchronize()
 lib.dl_debug_chain_prof(None)
-allb = buf.cpu().numpy()
-print('IN phase cycles (issue, data, a_empty, split, st+arrive):', allb[1000:1005])
-b = allb[:1024].view().reshape(8, 4, 32)
-t0 = b[0, 0, 0]
-names = {
-    0: {0: 'tile', 1: 'g0', 2: 'g1', 3: 'g2'},
-    1: {0: 'w.d1', 1: 'd1', 2: 'A2done', 3: 'u', 4: 'A3_0', 5: 'y0', 6: 'st0', 7: 'A3_1', 8: 'y1', 9: 'st1', 10: 'A3_2', 11: 'y2', 12: 'st2'},
-    2: {1: 's1g0', 2: 's1g1', 3: 's1g2', 8: 's2', 9: 'ac', 10: 's3o0', 11: 'au0', 12: 's3o1', 13: 'au1', 14: 's3o2', 15: 'au2'},
-    3: {0: 'tile'},
-}
-for it in range(2, 5):
-    print('tile', it)
-    for r, nm in zip(range(4), ['IN ', 'MID', 'MMA', 'LD ']):
-        print('  ', nm, ' '.join(f"{names[r][k]}={(b[it, r, k] - t0)}" for k in sorted(names[r]) if b[it, r, k]))
+b = buf.cpu().numpy()[:1024].reshape(8, 4, 32)
+t0 = min(v for v in b[2].ravel() if v)
+for it in range(2, 6):
+    ev = sorted((int(b[it, r, e]) - t0, r, e) for r in range(4) for e in range(32) if b[it, r, e])
+    print(f'tile {it}: ' + ' '.join(f'{r}.{e}@{t}' for t, r, e in ev))
+inr = buf.cpu().numpy()[1024:1024 + 32].reshape(8, 4)
+print('IN warps (chunks, wait_full, wait_aempty, work):')
+print(inr)
+m = buf.cpu().numpy()[1100:1108]
+print('MMA: total, idle_loops, gate_blocked_loops, s1_cycles, conv_cycles, items, tiles, s1_issue_only:', m)

@@ -7,7 +7,7 @@
 
 using namespace dl::umma;
 
-__global__ void rate_k(int mode, int N, int iters, long long* out) {
+__global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int acol) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tb_s;
@@ -20,7 +20,73 @@ __global__ void rate_k(int mode, int N, int iters, long long* out) {
   __syncthreads();
   fence_after();
   const uint32_t tb = tb_s;
-  if (mode >= 20) {
+  if (mode >= 40) {
+    // kernel-pattern probe: 6 TS MMAs (3x3 split pairs) per step, plus optional commit / fence / poll
+    __shared__ uint64_t mb2, mb3;
+    if (threadIdx.x == 0) { mbar_init(&mb2, 1); mbar_init(&mb3, 1); mbar_fence_init(); mbar_arrive(&mb3); }
+    __syncthreads();
+    const uint32_t sbb = smem_u32(smem + 32768);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    const int v = mode - 40;
+    if (warp == 0) {
+      uint64_t bd[3];
+      for (int j = 0; j < 3; ++j) bd[j] = desc_noswz(sbb + j * 1024, 128, 256);
+      long long t0 = clock64();
+      for (int k = 0; k < iters / 6; ++k) {
+        if (v & 4) { volatile bool r = mbar_test_warp(&mb3, 0); (void)r; }
+        if (v & 2) fence_after();
+        if (elect_one()) {
+          mma_ts(tb + dcol, tb + acol + 16, bd[0], id, k > 0);
+          mma_ts(tb + dcol, tb + acol + 8, bd[1], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[2], id, 1);
+          mma_ts(tb + dcol, tb + acol + 8, bd[0], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[1], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[0], id, 1);
+          if (v & 1) commit(&mb2);
+        }
+        __syncwarp();
+        for (int j = 0; j < 3; ++j) bd[j] += ((k & 7) == 7) ? (uint64_t)-14 : 2;
+      }
+      long long t1 = clock64();
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+      mbar_wait(&mbar, 0);
+      long long t2 = clock64();
+      if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+    }
+  } else if (mode >= 30) {
+    // warp 0 issues TS MMAs (D at dcol, A at acol); warps 4..7 generate TMEM traffic meanwhile:
+    // mode 30 none, 31 tcgen05.ld x16, 32 tcgen05.st x16, 33 both
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+    const uint32_t sbb = smem_u32(smem + 32768);
+    const uint64_t bd = desc_noswz(sbb, 128, 256);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    if (warp == 0) {
+      long long t0 = clock64();
+      for (int k = 0; k < iters; ++k) {
+        if (elect_one()) mma_ts(tb + (uint32_t)dcol, tb + (uint32_t)acol, bd, id, 1);
+        __syncwarp();
+      }
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+      mbar_wait(&mbar, 0);
+      long long t1 = clock64();
+      if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; stop = 1; }
+    } else if (warp >= 4) {
+      const uint32_t ta = tb + ((uint32_t)(32 * (warp & 3)) << 16) + 480u;
+      uint32_t r[16];
+      for (int i = 0; i < 16; ++i) r[i] = i;
+      long long n = 0;
+      while (!stop) {
+        if (mode & 1) { tmem_ld<16>(ta, r); tmem_wait_ld(); }
+        if (mode & 2) { tmem_st<16>(ta + 16, r); tmem_wait_st(); }
+        ++n;
+      }
+      if ((threadIdx.x & 31) == 0 && warp == 4) out[1] = n;
+    }
+  } else if (mode >= 20) {
     // (mode - 20) issuing warps, each its own accumulator, iters/W MMAs each
     const int W = mode - 20;
     const uint32_t sa = smem_u32(smem), sbb = smem_u32(smem + 32768);
@@ -86,11 +152,11 @@ __global__ void rate_k(int mode, int N, int iters, long long* out) {
   if (warp == 0) tmem_dealloc(tb, 512);
 }
 
-extern "C" int mma_rate(int mode, int N, int iters, long long* out_host) {
+extern "C" int mma_rate(int mode, int N, int iters, long long* out_host, int dcol, int acol) {
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  rate_k<<<1, 128, 64 * 1024>>>(mode, N, iters, d);
+  rate_k<<<1, 256, 64 * 1024>>>(mode, N, iters, d, dcol, acol);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(out_host, d, 16, cudaMemcpyDeviceToHost);
   cudaFree(d);
