@@ -106,6 +106,15 @@ __device__ __forceinline__ void ld16f(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 channel rows of one voxel -> HBM (row stride `stride` floats), streaming stores
+__device__ __forceinline__ void store16(float* d, int64_t stride, const float (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    __stcs(d, v[i]);
+    d += stride;
+  }
+}
+
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
@@ -297,11 +306,12 @@ struct Chain3 {
   CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
   const float* in;
   float* out;
+  float* mid;                         // optional: stage-1 accumulator D1 (G1*N1 padded rows) -> HBM
   const float* bias2;                 // real stage-2 bias per (group, channel < C2) or null
   const uint16_t* w1;                 // images, part-major: (q * groups + g) * img_bytes
   const uint16_t* w2;
   const uint16_t* w3;
-  int64_t nbatch, nvox, in_bs, out_bs, tiles_per_b;
+  int64_t nbatch, nvox, in_bs, out_bs, mid_bs, tiles_per_b;
   int G1, C1, K1, N1;                 // stage 1: groups, real in-ch/group, padded K, padded N
   int G2, C2, N2;                     // stage 2: groups, real out-ch/group, padded N
   int C3, N3;                         // stage 3: real / padded out-ch per group
@@ -420,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
       for (int ck = cg; ck < D1w / 16; ck += 2) {
         float vv[16];
         ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
+        if (p.mid && vok) store16(p.mid + b * p.mid_bs + (int64_t)ck * 16 * stride + v, stride, vv);
         split_store16<PARTS>(tq + p.colA2 + (uint32_t)ck * 8, D1w / 2, vv);
       }
       tmem_wait_st();
@@ -707,6 +718,8 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     uint32_t cslot = (uint32_t)(cw % p.NAc), cround = (uint32_t)(cw / p.NAc), it = 0;
     int i0 = cw;   // first item of this warp in the current tile
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int64_t b = t / p.tiles_per_b, vx = (t - b * p.tiles_per_b) * kTileV + 32 * (warp & 3) + lane;
+      const bool vok = vx < p.nvox;
       if (warp == kIN3) DL_PROF(1, 0);
       mbar_wait_warp(&bars.d1_full, it & 1);
       if (warp == kIN3) DL_PROF(1, 1);
@@ -717,6 +730,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         float v[16];
         if (i < nk2) {
           ld16f(tq + p.colD1 + (uint32_t)i * 16, v);
+          if (p.mid && vok) store16(p.mid + b * p.mid_bs + (int64_t)i * 16 * p.nvox + vx, p.nvox, v);
         } else {
           if (!d2_seen) {
             if (warp == kIN3) DL_PROF(1, 2);
@@ -895,66 +909,64 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 }
 
 // ============================================================================ LSC weight Gram
+// G[j][i] = sum_v g_v[j] c_v[i] over this CTA's voxels, where c = M x (saved by the forward as its
+// stage-1 accumulator) and g = B'^T dy (written by the adjoint chain kernel the same way); both are
+// fp32 (B, rows, V) tensors with per-shell rows padded to 16 (padding rows are exact zeros).
+// 64-voxel tiles: a TMA ring streams 16-row x 68-voxel blocks; eight MID warps split each value into
+// two bf16 terms and write SWIZZLE_128B K-major operand tiles (row = channel, K = voxel), double
+// buffered, so the MMA warp's Gram of tile t overlaps the conversion of tile t+1.  The bias gradient
+// db[o] = sum_v beta . g_v[o] is summed from the fp32 values on the way.
+constexpr int kGV = 64;                         // voxels per Gram tile (one 128-byte K atom of bf16)
+constexpr int kGBoxV = kGV + 4;                 // TMA box width (16-byte realignment margin)
+constexpr int kGStage = 16 * kGBoxV * 4;        // ring stage: 16 rows x 68 voxels fp32
+constexpr int kGMID = 8;
+constexpr int kGWarpMMA = kGMID;
+constexpr int kGWarpLD = kGMID + 1;
+constexpr int kGThreads = (kGWarpLD + 1) * 32;
+
 struct GramP {
-  CUtensorMap tm[2];         // channel-pair views of dy (0) and x (1)
-  const float* x;
-  const float* dy;
-  const uint16_t* wM;        // M images (rows RPi, cols NPi), PARTS x groups
-  const uint16_t* wB;        // B' images (rows NPo, cols RPo), PARTS
+  CUtensorMap tm[2];         // channel-pair views of g (0) and c (1)
+  const float* g;
+  const float* c;
   const float* beta;         // R_out
   float* partials;           // [grid][GR*GC] then db [grid][S_out]
-  int64_t nbatch, nvox, x_bs, dy_bs, tiles_per_b;
-  int S_in, N, NPi, RPi, S_out, N_out, NPo, RPo, R_out;
-  int wM_groups;
-  int NA, ns, tma;
-  uint32_t wM_img, wB_img;
-  uint32_t sm_wM, sm_wB, sm_c, sm_g, sm_beta, sm_ring, sm_bar, smem_bytes, ctile, gtile;   // per-part tile bytes
-  uint32_t colGA, colGB, colGC, colA, colDg, colDc;
-  int GR, GC;                // g rows (S_out*RPo), c rows (S_in*RPi)
+  int64_t nbatch, nvox, g_bs, c_bs, tiles_per_b;
+  int GR, GC, S_out, RPo, R_out;
+  int tma, ns;
+  uint32_t sm_buf0, buf_bytes, cpart, gpart;   // buffer b at sm_buf0 + b*buf_bytes: c part0|c part1|g part0|g part1
+  uint32_t sm_beta, sm_ring, sm_bar, smem_bytes;
+  uint32_t colGA, colGB, colGC;
 };
 
 struct BarsG {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
-  uint64_t dg_full, dg_free, dc_full, dc_free, tiles_full, gram_done;
+  uint64_t tiles_full[2], gram_done[2];
   float db[4];
   uint32_t tmem_base;
 };
 
-template <int PARTS, int NS>
-__global__ void __launch_bounds__(kThreads, 1) gram_tc(const __grid_constant__ GramP p) {
+template <int NS>
+__global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ GramP p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t kSlotW = PARTS * 8;
   {
-    const uint32_t bM = (uint32_t)PARTS * p.wM_groups * p.wM_img, bB = (uint32_t)PARTS * p.wB_img;
-    const uint4 *sM = reinterpret_cast<const uint4*>(p.wM), *sB = reinterpret_cast<const uint4*>(p.wB);
-    uint4 *dM = reinterpret_cast<uint4*>(smem + p.sm_wM), *dB = reinterpret_cast<uint4*>(smem + p.sm_wB);
-    for (uint32_t i = threadIdx.x; i < bM / 16; i += blockDim.x) dM[i] = __ldg(sM + i);
-    for (uint32_t i = threadIdx.x; i < bB / 16; i += blockDim.x) dB[i] = __ldg(sB + i);
-    // operand tiles (and the margin block C over-reads) start zeroed: padding rows stay finite
-    uint4* z = reinterpret_cast<uint4*>(smem + p.sm_c);
-    for (uint32_t i = threadIdx.x; i < (p.sm_beta - p.sm_c) / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    // operand tiles start zeroed: g rows GR..127 (block A's M padding) are never written
+    uint4* z = reinterpret_cast<uint4*>(smem + p.sm_buf0);
+    for (uint32_t i = threadIdx.x; i < 2 * p.buf_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     float* sb = reinterpret_cast<float*>(smem + p.sm_beta);
     for (int i = threadIdx.x; i < p.RPo; i += blockDim.x) sb[i] = i < p.R_out ? __ldg(p.beta + i) : 0.f;
   }
-  if (warp == kWarpMMA) tmem_alloc(&bars.tmem_base, 512);
+  if (warp == kGWarpMMA) tmem_alloc(&bars.tmem_base, 256);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], kIN);
+      mbar_init(&bars.empty[s], kGMID);
     }
-    for (int s = 0; s < p.NA; ++s) {
-      mbar_init(&bars.a_full[s], 4);   // one arrival per TMEM lane quadrant
-      mbar_init(&bars.a_empty[s], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.tiles_full[b], kGMID);
+      mbar_init(&bars.gram_done[b], 1);
     }
-    mbar_init(&bars.dg_full, 1);
-    mbar_init(&bars.dg_free, kMID);
-    mbar_init(&bars.dc_full, 1);
-    mbar_init(&bars.dc_free, kMID);
-    mbar_init(&bars.tiles_full, kMID);
-    mbar_init(&bars.gram_done, 1);
     for (int o = 0; o < 4; ++o) bars.db[o] = 0.f;
     mbar_fence_init();
   }
@@ -964,100 +976,84 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const __grid_constant__ G
   fence_after();
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
-  const int nkg = p.NPo / 16, nkc = p.NPi / 16;
+  const int nG = p.GR / 16, nC = p.GC / 16, per_tile = nG + nC;
 
-  // chunk sequence per tile: dy groups (S_out x nkg chunks), then x groups (S_in x nkc chunks)
-  const int ng = p.S_out * nkg, per_tile = ng + p.S_in * nkc;
-  auto geo = [&](int r) {
-    const bool pass = r >= ng;
-    const int rr = pass ? r - ng : r, nk = pass ? nkc : nkg, g = rr / nk, k = rr - g * nk;
-    const int C = pass ? p.N : p.N_out;
-    return ChunkGeo{pass ? 1 : 0, g * C + 16 * k, C - 16 * k};
-  };
-  if (warp < kIN) {
-    const uint32_t tslots = tbase + ((uint32_t)(32 * warp) << 16) + p.colA;
-    if (p.tma) {
-      in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
-                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty);
-    } else {
-      const float* const base[2] = {p.dy, p.x};
-      const int64_t bs[2] = {p.dy_bs, p.x_bs};
-      in_role_cpasync<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots, p.NA, bars.a_full,
-                                 bars.a_empty, reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
-    }
-  } else if (warp < kWarpMMA) {
-    const int mw = warp - kIN, qd = mw & 3, cg = mw >> 2;
-    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
-    const int row = 32 * qd + lane;
-    const int grow = p.GR < 128 ? 128 : p.GR;
-    float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
-    // SWIZZLE_128B offsets of this thread's voxel (K index = row): the K-atom / in-row part is fixed,
-    // the 16-byte chunk is XOR-ed with the row-in-group m = j & 7
-    const uint32_t gk = (uint32_t)(row >> 6) * (uint32_t)(grow >> 3) * 1024u + (uint32_t)(row & 7) * 2u;
-    const uint32_t ck_ = (uint32_t)(row >> 6) * (uint32_t)(p.GC >> 3) * 1024u + (uint32_t)(row & 7) * 2u;
-    uint32_t xo[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) xo[m] = (uint32_t)m * 128u + ((uint32_t)(((row & 63) >> 3) ^ m) << 4);
+  if (warp < kGMID) {
+    // =========================== MID: fp32 rows -> two-term bf16 SW128 tiles ===========================
     const float* sbeta = reinterpret_cast<const float*>(smem + p.sm_beta);
-    uint32_t it = 0;
+    const int sh = (int)(p.nvox & 3);
+    float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t s = 0, round = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      // ---- g -> two-term SW128 tile (+ beta . g for the bias gradient) ----
-      mbar_wait_warp(&bars.dg_full, it & 1);
-      if (it > 0) mbar_wait_warp(&bars.gram_done, (it - 1) & 1);   // previous Gram finished reading the tiles
-      fence_after();
-      for (int ck = cg; ck < p.GR / 16; ck += kMID / 4) {
-        float vv[16];
-        ld16f(tq + p.colDg + (uint32_t)ck * 16, vv);
-        const int o = (ck * 16) / p.RPo, r0 = ck * 16 - o * p.RPo;   // RPo % 16 == 0: one shell per chunk
-        float sdb = 0.f;
+      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kGV;
+      const uint32_t buf = it & 1;
+      if (it >= 2) mbar_wait_warp(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
+      uint8_t* tb = smem + p.sm_buf0 + buf * p.buf_bytes;
+      const bool ok0 = v0 + 2 * lane < p.nvox, ok1 = v0 + 2 * lane + 1 < p.nvox;
+      for (int r = 0; r < per_tile; ++r) {
+        const bool isg = r < nG;
+        const int row0 = 16 * (isg ? r : r - nG);
+        float x[2][2];   // two rows of this warp, two voxels of this lane
+        if (p.tma) {
+          mbar_wait_warp(&bars.full[s], round & 1);
+          const float* st = reinterpret_cast<const float*>(smem + p.sm_ring + s * kGStage);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) sdb += sbeta[r0 + i] * vv[i];
+          for (int h = 0; h < 2; ++h) {
+            const int j = 2 * warp + h;   // row within the chunk; even rows in box 0, odd in box 1
+            const float2 v2 = *reinterpret_cast<const float2*>(st + (j & 1) * (8 * kGBoxV + sh) + (j >> 1) * kGBoxV +
+                                                               2 * lane);
+            x[h][0] = ok0 ? v2.x : 0.f;
+            x[h][1] = ok1 ? v2.y : 0.f;
+          }
+          warp_arrive(&bars.empty[s]);
+          if (++s == NS) {
+            s = 0;
+            ++round;
+          }
+        } else {
+          const float* src = isg ? p.g + b * p.g_bs : p.c + b * p.c_bs;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == o) dbacc[q] += sdb;
-        uint8_t* t0 = smem + p.sm_g + gk + (uint32_t)ck * 2048u;
+          for (int h = 0; h < 2; ++h) {
+            const float* rp = src + (int64_t)(row0 + 2 * warp + h) * p.nvox + v0 + 2 * lane;
+            x[h][0] = ok0 ? __ldg(rp) : 0.f;
+            x[h][1] = ok1 ? __ldg(rp + 1) : 0.f;
+          }
+        }
+        uint8_t* part0 = tb + (isg ? 2 * p.cpart : 0);
+        const uint32_t pstride = isg ? p.gpart : p.cpart;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
-          const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
-          const uint32_t off = (uint32_t)(i >> 3) * 1024u + xo[i & 7];
-          *reinterpret_cast<uint16_t*>(t0 + off) = (uint16_t)pk0;
-          *reinterpret_cast<uint16_t*>(t0 + p.gtile + off) = (uint16_t)pk1;
+        for (int h = 0; h < 2; ++h) {
+          const int row = row0 + 2 * warp + h;
+          const uint32_t hi = pack_bf16x2(x[h][0], x[h][1]);
+          const uint32_t lo = pack_bf16x2(x[h][0] - bf16lo_to_f32(hi), x[h][1] - bf16hi_to_f32(hi));
+          const uint32_t off = (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
+                               ((uint32_t)((lane >> 2) ^ (row & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
+          *reinterpret_cast<uint32_t*>(part0 + off) = hi;
+          *reinterpret_cast<uint32_t*>(part0 + pstride + off) = lo;
+          if (isg) {
+            const int o = row / p.RPo;
+            const float bt = sbeta[row - o * p.RPo] * (x[h][0] + x[h][1]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q == o) dbacc[q] += bt;
+          }
         }
       }
-      fence_before();
-      warp_arrive(&bars.dg_free);
-      // ---- c -> two-term SW128 tile ----
-      mbar_wait_warp(&bars.dc_full, it & 1);
-      fence_after();
-      for (int ck = cg; ck < p.GC / 16; ck += kMID / 4) {
-        float vv[16];
-        ld16f(tq + p.colDc + (uint32_t)ck * 16, vv);
-        uint8_t* t0 = smem + p.sm_c + ck_ + (uint32_t)ck * 2048u;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t pk0 = pack_bf16x2(vv[i], 0.f);
-          const uint32_t pk1 = pack_bf16x2(vv[i] - bf16lo_to_f32(pk0), 0.f);
-          const uint32_t off = (uint32_t)(i >> 3) * 1024u + xo[i & 7];
-          *reinterpret_cast<uint16_t*>(t0 + off) = (uint16_t)pk0;
-          *reinterpret_cast<uint16_t*>(t0 + p.ctile + off) = (uint16_t)pk1;
-        }
-      }
-      fence_before();
-      warp_arrive(&bars.dc_free);
-      fence_proxy_async();
-      warp_arrive(&bars.tiles_full);
+      fence_proxy_async();   // generic-proxy tile writes -> visible to the tensor core
+      warp_arrive(&bars.tiles_full[buf]);
     }
-    if (it > 0) mbar_wait_warp(&bars.gram_done, (it - 1) & 1);
+    // ---- this CTA's Gram partial (after the last Gram MMA) ----
+    if (it > 0) mbar_wait_warp(&bars.gram_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
     fence_after();
-    // ---- this CTA's Gram partial: G[j (g row)][i (c row)] ----
+    const int qd = warp & 3, cg = warp >> 2, row = 32 * qd + lane;
+    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
     float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
-    for (int ck = cg; ck < p.GC / 16; ck += kMID / 4) {       // block A: lane = g row
+    for (int ck = cg; ck < p.GC / 16; ck += 2) {   // block A: lane = g row, column = c row
       float vv[16];
       ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
       if (row < p.GR)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = vv[i];
+        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = it > 0 ? vv[i] : 0.f;
     }
     if (p.GR > 128 && cg == 0) {
       float vv[16];
@@ -1065,100 +1061,90 @@ __global__ void __launch_bounds__(kThreads, 1) gram_tc(const __grid_constant__ G
       if (row < p.GC)
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = vv[c];
+          if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = it > 0 ? vv[c] : 0.f;
       if (p.GC > 128 && qd == 0) {
         ld16f(tq + p.colGC, vv);   // block C (M = 64): lanes 0..15 = c rows 128..143
         if (lane < 16 && 128 + lane < p.GC)
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = vv[c];
+            if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = it > 0 ? vv[c] : 0.f;
       }
     }
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
-      float s = dbacc[o];
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0 && o < p.S_out) atomicAdd(&bars.db[o], s);
+      float v = dbacc[o];
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0 && o < p.S_out) atomicAdd(&bars.db[o], v);
     }
-    named_sync(1, kMID * 32);
-    if (mw == 0 && lane == 0) {
+    named_sync(1, kGMID * 32);
+    if (warp == 0 && lane == 0) {
       float* dbp = p.partials + (int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out;
       for (int o = 0; o < p.S_out; ++o) dbp[o] = bars.db[o];
     }
-  } else if (warp == kWarpMMA) {
-    const uint32_t sM = smem_u32(smem + p.sm_wM), sB = smem_u32(smem + p.sm_wB);
-    const uint32_t sc = smem_u32(smem + p.sm_c), sg = smem_u32(smem + p.sm_g);
-    const uint32_t idg = idesc_bf16(128, p.RPo, 0, 1);   // g: A = dy (TMEM), B = B' image MN-major
-    const uint32_t idc = idesc_bf16(128, p.RPi, 0, 0);   // c: B = M image K-major
+  } else if (warp == kGWarpMMA) {
+    // =========================== MMA: G += g^T c per 16-voxel K-step, three blocks ===========================
     const uint32_t idA = idesc_bf16(128, p.GC, 0, 0), idB = idesc_bf16(128, 16, 0, 0), idC = idesc_bf16(64, 16, 0, 0);
-    const int grow = p.GR < 128 ? 128 : p.GR;
-    const uint32_t ASg = (uint32_t)(grow / 8) * 1024u, ASc = (uint32_t)(p.GC / 8) * 1024u;
-    const uint64_t ksg = wkstep(p.RPo, 0), ksc = wkstep(p.NPi, 1);
-    uint32_t aslot = 0, around = 0, it = 0;
+    const uint32_t base = smem_u32(smem + p.sm_buf0);
+    uint32_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      for (int pass = 0; pass < 2; ++pass) {
-        if (it > 0) {
-          mbar_wait_warp(pass ? &bars.dc_free : &bars.dg_free, (it - 1) & 1);
-          fence_after();
-        }
-        const int G = pass ? p.S_in : p.S_out, nk = pass ? nkc : nkg;
-        for (int g = 0; g < G; ++g) {
-          uint64_t bd[PARTS];
-          const int wg = p.wM_groups > 1 ? g : 0;
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j)
-            bd[j] = pass ? wdesc(sM + (uint32_t)(j * p.wM_groups + wg) * p.wM_img, p.NPi, 1, 0)
-                         : wdesc(sB + (uint32_t)j * p.wB_img, p.RPo, 0, 0);
-          const uint32_t d = tbase + (pass ? p.colDc + (uint32_t)(g * p.RPi) : p.colDg + (uint32_t)(g * p.RPo));
-          for (int k = 0; k < nk; ++k) {
-            mbar_wait_warp(&bars.a_full[aslot], around & 1);
-            fence_after();
-            if (elect_one()) {
-              kstep_ts<PARTS>(d, tbase + p.colA + aslot * kSlotW, 8, bd, pass ? idc : idg, k == 0);
-              commit(&bars.a_empty[aslot]);
-              if (k == nk - 1 && g == G - 1) commit(pass ? &bars.dc_full : &bars.dg_full);
-            }
-            __syncwarp();
-            if (++aslot == (uint32_t)p.NA) {
-              aslot = 0;
-              ++around;
-            }
-#pragma unroll
-            for (int j = 0; j < PARTS; ++j) bd[j] += pass ? ksc : ksg;
-          }
-        }
-      }
-      // ---- Gram over this tile's 128 voxels (two-term split operands, three blocks) ----
-      mbar_wait_warp(&bars.tiles_full, it & 1);
+      const uint32_t buf = it & 1;
+      mbar_wait_warp(&bars.tiles_full[buf], (it >> 1) & 1);
       fence_after();
-      for (int kk = 0; kk < kTileV / 16; ++kk) {
-        const uint32_t ko = (uint32_t)(kk >> 2), kb = (uint32_t)(kk & 3) * 32u;
+      const uint32_t c0 = base + buf * p.buf_bytes, g0 = c0 + 2 * p.cpart;
+      for (int kk = 0; kk < kGV / 16; ++kk) {
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
             const int i = Pairs<2>::i(k), j = Pairs<2>::j(k);
-            const uint32_t gI = sg + (uint32_t)i * p.gtile + ko * ASg + kb, gJ = sg + (uint32_t)j * p.gtile + ko * ASg + kb;
-            const uint32_t cI = sc + (uint32_t)i * p.ctile + ko * ASc + kb, cJ = sc + (uint32_t)j * p.ctile + ko * ASc + kb;
+            const uint32_t gI = g0 + (uint32_t)i * p.gpart + kk * 32u, gJ = g0 + (uint32_t)j * p.gpart + kk * 32u;
+            const uint32_t cI = c0 + (uint32_t)i * p.cpart + kk * 32u, cJ = c0 + (uint32_t)j * p.cpart + kk * 32u;
             const uint32_t acc = (it > 0 || kk > 0 || k > 0) ? 1u : 0u;
             mma_ss(tbase + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
             if (p.GR > 128) {
               mma_ss(tbase + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
               if (p.GC > 128)
-                mma_ss(tbase + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC, acc);
+                mma_ss(tbase + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC,
+                       acc);
             }
           }
         }
         __syncwarp();
       }
-      if (elect_one()) commit(&bars.gram_done);
+      if (elect_one()) commit(&bars.gram_done[buf]);
       __syncwarp();
     }
   } else if (p.tma) {
-    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
+    // =========================== TMA loader ===========================
+    if (elect_one()) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[0]) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[1]) : "memory");
+    }
+    __syncwarp();
+    const int sh = (int)(p.nvox & 3);
+    uint32_t s = 0, round = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b;
+      const int v0 = (int)((t - b * p.tiles_per_b) * kGV);
+      for (int r = 0; r < per_tile; ++r) {
+        const int tensor = r < nG ? 0 : 1, j0 = 8 * (r < nG ? r : r - nG);
+        if (round > 0) mbar_wait_warp(&bars.empty[s], (round - 1) & 1);
+        if (elect_one()) {
+          uint8_t* dst = smem + p.sm_ring + s * kGStage;
+          mbar_arrive_tx(&bars.full[s], kGStage);
+          tma_load_3d(dst, &p.tm[tensor], v0, j0, (int)b, &bars.full[s]);
+          tma_load_3d(dst + kGStage / 2, &p.tm[tensor], (int)p.nvox + v0 - sh, j0, (int)b, &bars.full[s]);
+        }
+        __syncwarp();
+        if (++s == NS) {
+          s = 0;
+          ++round;
+        }
+      }
+    }
   }
   fence_before();
   __syncthreads();
-  if (warp == kWarpMMA) tmem_dealloc(tbase, 512);
+  if (warp == kGWarpMMA) tmem_dealloc(tbase, 256);
 }
 
 // ---------------------------------------------------------------------------- operand packing
@@ -1397,35 +1383,21 @@ bool use_v3() {
   return v;
 }
 
-bool plan_gram(GramP& p, int parts) {
-  p.GR = p.S_out * p.RPo;
-  p.GC = p.S_in * p.RPi;
-  if (p.GR > 144 || p.GC > 144 || p.S_out > 4) return false;
-  const int grow = p.GR < 128 ? 128 : p.GR, slotw = parts * 8;
+bool plan_gram(GramP& p) {
+  if (p.GR > 144 || p.GC > 144 || p.S_out > 4 || p.GR % 16 || p.GC % 16) return false;
+  const int grow = p.GR < 128 ? 128 : p.GR;
   p.colGA = 0;
-  p.colGB = p.GC;
-  p.colGC = p.GC + 16;
-  const int col = p.GC + 32;
-  p.NA = (512 - col - p.GR - p.GC) / slotw;
-  if (p.NA > kMaxSlots) p.NA = kMaxSlots;
-  if (p.NA < 2) return false;
-  p.colA = col;
-  p.colDg = p.colA + p.NA * slotw;
-  p.colDc = p.colDg + p.GR;
-  p.wM_img = (uint32_t)(p.RPi * p.NPi * 2);
-  p.wB_img = (uint32_t)(p.NPo * p.RPo * 2);
-  p.ctile = (uint32_t)(p.GC / 8) * 1024u * 2u;
-  p.gtile = (uint32_t)(grow / 8) * 1024u * 2u;
+  p.colGB = (uint32_t)p.GC;
+  p.colGC = (uint32_t)p.GC + 16;
+  p.cpart = (uint32_t)(p.GC / 8) * 1024u;
+  p.gpart = (uint32_t)(grow / 8) * 1024u;
+  p.buf_bytes = 2 * p.cpart + 2 * p.gpart;   // block C over-reads c rows up to 191: they land in what follows
   size_t o = 0;
-  p.sm_wM = (uint32_t)o; o = al(o + (size_t)parts * p.wM_groups * p.wM_img, 1024);
-  p.sm_wB = (uint32_t)o; o = al(o + (size_t)parts * p.wB_img, 1024);
-  p.sm_c = (uint32_t)o; o = al(o + (size_t)2 * p.ctile, 1024);
-  // block C reads c rows up to 191 of every K-atom: they land in the g tile that follows c
-  p.sm_g = (uint32_t)o; o = al(o + (size_t)2 * p.gtile, 1024);
+  p.sm_buf0 = (uint32_t)o; o = al(o + 2 * (size_t)p.buf_bytes + 8192, 1024);
   p.sm_beta = (uint32_t)o; o = al(o + (size_t)p.RPo * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (p.ns = 8; p.ns >= 2; p.ns /= 2) {
-    size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
+  for (p.ns = kMaxStages; p.ns >= 2; --p.ns) {
+    size_t q = al(p.sm_ring + (size_t)p.ns * kGStage, 16);
     p.sm_bar = (uint32_t)q;
     q = al(q + sizeof(BarsG), 16);
     p.smem_bytes = (uint32_t)q;
@@ -1470,12 +1442,23 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
   return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
 }
 
-template <int PARTS>
-int run_gram(const GramP& p, int grid, cudaStream_t st) {
-  auto k = p.ns == 8 ? gram_tc<PARTS, 8> : p.ns == 4 ? gram_tc<PARTS, 4> : gram_tc<PARTS, 2>;
-  DL_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
-  k<<<grid, kThreads, p.smem_bytes, st>>>(p);
+template <int NS>
+int launch_gram(const GramP& p, int grid, cudaStream_t st) {
+  DL_CUDA(cudaFuncSetAttribute(gram_tc<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+  gram_tc<NS><<<grid, kGThreads, p.smem_bytes, st>>>(p);
   return after_launch("gram_tc");
+}
+
+int run_gram(const GramP& p, int grid, cudaStream_t st) {
+  switch (p.ns) {
+    case 2: return launch_gram<2>(p, grid, st);
+    case 3: return launch_gram<3>(p, grid, st);
+    case 4: return launch_gram<4>(p, grid, st);
+    case 5: return launch_gram<5>(p, grid, st);
+    case 6: return launch_gram<6>(p, grid, st);
+    case 7: return launch_gram<7>(p, grid, st);
+    default: return launch_gram<8>(p, grid, st);
+  }
 }
 
 int pack(const float* W, uint16_t* out, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp, int parts,
@@ -1528,15 +1511,15 @@ GramP gram_params(const Dims& d, const WsLayout& w, uint8_t* ws) {
   GramP p{};
   p.nbatch = d.nbatch;
   p.nvox = d.nvox;
-  p.tiles_per_b = (d.nvox + kTileV - 1) / kTileV;
-  p.S_in = d.s_in; p.N = d.n; p.NPi = d.NPi; p.RPi = d.RPi;
-  p.S_out = d.s_out; p.N_out = d.n_out; p.NPo = d.NPo; p.RPo = d.RPo; p.R_out = d.r_out;
-  p.wM_groups = d.mg;
-  p.wM = reinterpret_cast<const uint16_t*>(ws + w.imgM);
-  p.wB = reinterpret_cast<const uint16_t*>(ws + w.imgB);
+  p.tiles_per_b = (d.nvox + kGV - 1) / kGV;
+  p.GR = d.s_out * d.RPo;
+  p.GC = d.s_in * d.RPi;
+  p.S_out = d.s_out;
+  p.RPo = d.RPo;
+  p.R_out = d.r_out;
   p.partials = reinterpret_cast<float*>(ws + w.parts);
-  p.x_bs = (int64_t)d.s_in * d.n * d.nvox;
-  p.dy_bs = (int64_t)d.s_out * d.n_out * d.nvox;
+  p.g_bs = (int64_t)p.GR * d.nvox;
+  p.c_bs = (int64_t)p.GC * d.nvox;
   return p;
 }
 
@@ -1548,13 +1531,14 @@ bool chain_fits(const Dims& d) {
     Chain3 v = c;
     return (use_v3() && plan_chain3v(v, d.parts)) || plan_chain3(c, d.parts);
   };
-  return fits(f) && fits(a) && plan_gram(g, d.parts);
+  return fits(f) && fits(a) && plan_gram(g);
 }
 
 // Channel-pair view of a (nbatch, rows, nvox) fp32 tensor for TMA: element (u, j, b) is channel 2j + u / nvox,
 // voxel u % nvox -- rows 2j and 2j+1 are contiguous, so the row stride 8*nvox bytes is 16-byte aligned for
 // any even nvox.  Box = 132 voxels x 8 channel pairs.  False (use the cp.async path) if not expressible.
-bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, int64_t group_rows, int64_t nvox) {
+bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, int64_t group_rows, int64_t nvox,
+              int boxv = kBoxV) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1570,7 +1554,7 @@ bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, i
     return false;
   const cuuint64_t dims[3] = {(cuuint64_t)(2 * nvox), (cuuint64_t)(rows / 2), (cuuint64_t)nbatch};
   const cuuint64_t strides[2] = {(cuuint64_t)(8 * nvox), (cuuint64_t)(4 * rows * nvox)};
-  const cuuint32_t box[3] = {(cuuint32_t)kBoxV, 8u, 1u};
+  const cuuint32_t box[3] = {(cuuint32_t)boxv, 8u, 1u};
   const cuuint32_t es[3] = {1u, 1u, 1u};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1609,9 +1593,11 @@ size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int
   return ws_layout(make_dims(nbatch, s_in, s_out, n, r_in, r_out, n_out, nvox, 1), kMaxParts).total;
 }
 
-int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, const float* L, const float* bvec,
-                     const float* Bt, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n,
-                     int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+int64_t dl_chain_mid_rows(int64_t shells, int64_t r) { return shells * ((r + 15) / 16 * 16); }
+
+int dl_chain_fwd_f32(const float* x, float* y, float* c_mid, const float* M, int m_per_shell, const float* L,
+                     const float* bvec, const float* Bt, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out,
+                     int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   using namespace dl::tc;
   dl::begin_call();
   int sm = 0;
@@ -1629,6 +1615,8 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
   p.in = x;
   p.out = y;
+  p.mid = c_mid;
+  p.mid_bs = (int64_t)d.s_in * d.RPi * nvox;
   p.bias2 = bvec;
   p.prof = g_prof;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
@@ -1636,45 +1624,49 @@ int dl_chain_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, 
   return run_chain(p, d, grid, st, "chain_fwd");
 }
 
-int dl_chain_bwd_f32(const float* x, const float* dy, float* dx, float* dW, float* db, const float* M, int m_per_shell,
-                     const float* L, const float* Bt, const float* P, const float* beta, void* workspace,
-                     int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K, int64_t n, int64_t r_in, int64_t r_out,
-                     int64_t n_out, int64_t nvox, void* stream) {
+int dl_chain_bwd_f32(const float* c_mid, const float* dy, float* dx, float* dW, float* db, float* g_mid,
+                     const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
+                     const float* beta, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K,
+                     int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   using namespace dl::tc;
   dl::begin_call();
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
-  DL_REQUIRE(dy && M && Bt && workspace, "chain_bwd: null pointer");
-  DL_REQUIRE(!dx || L, "chain_bwd: dx needs L");
-  DL_REQUIRE(!(dW || db) || (x && P && beta), "chain_bwd: weight grad needs x, P, beta");
+  DL_REQUIRE(dy && dx && M && L && Bt && workspace, "chain_bwd: null pointer");
+  DL_REQUIRE(!(dW || db) || (c_mid && g_mid && P && beta), "chain_bwd: the weight gradient needs c_mid, g_mid, P, beta");
   Dims d = make_dims(nbatch, s_in, s_out, n, r_in, r_out, n_out, nvox, m_per_shell);
+  DL_REQUIRE(chain_fits(d), "chain_bwd: channel counts exceed the fused kernel's TMEM/smem plan");
   WsLayout w = ws_layout(d, kMaxParts);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   cudaStream_t st = dl::as_stream(stream);
   const int64_t ntiles = nbatch * ((nvox + kTileV - 1) / kTileV);
-  DL_TRY(pack_all(d, w, ws, M, dx ? L : nullptr, Bt, st));
-  if (dx && ntiles > 0) {
+  const bool wgrad = dW || db;
+  DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
+  if (ntiles > 0) {
+    // adjoint chain dy -> dx; its stage-1 accumulator g = B'^T dy goes to g_mid for the Gram
     Chain3 p = chain3_params(d, w, ws, true);
     p.in = dy;
     p.out = dx;
+    p.mid = wgrad ? g_mid : nullptr;
+    p.mid_bs = (int64_t)d.s_out * d.RPo * nvox;
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
-    const int grid = grid_for(ntiles, sm);
-    DL_TRY(run_chain(p, d, grid, st, "chain_bwd"));
+    DL_TRY(run_chain(p, d, grid_for(ntiles, sm), st, "chain_bwd"));
   }
-  if (dW || db) {
+  if (wgrad) {
     GramP g = gram_params(d, w, ws);
-    DL_REQUIRE(plan_gram(g, d.parts), "chain_bwd: channel counts exceed the fused Gram plan");
+    DL_REQUIRE(plan_gram(g), "chain_bwd: channel counts exceed the fused Gram plan");
     const int GR = g.GR, GC = g.GC;
+    const int64_t gtiles = nbatch * g.tiles_per_b;
     int nparts = 0;
-    if (ntiles > 0) {
-      g.x = x;
-      g.dy = dy;
+    if (gtiles > 0) {
+      g.g = g_mid;
+      g.c = c_mid;
       g.beta = beta;
-      g.tma = !tma_disabled() && pair_map(&g.tm[0], dy, nbatch, s_out * n_out, n_out, nvox) &&
-              pair_map(&g.tm[1], x, nbatch, s_in * n, n, nvox);
-      nparts = grid_for(ntiles, sm < kMaxParts ? sm : kMaxParts);
-      DL_TRY(d.parts == 3 ? run_gram<3>(g, nparts, st) : run_gram<2>(g, nparts, st));
+      g.tma = !tma_disabled() && pair_map(&g.tm[0], g_mid, nbatch, GR, d.RPo, nvox, kGBoxV) &&
+              pair_map(&g.tm[1], c_mid, nbatch, GC, d.RPi, nvox, kGBoxV);
+      nparts = grid_for(gtiles, sm < kMaxParts ? sm : kMaxParts);
+      DL_TRY(run_gram(g, nparts, st));
     }
     float* partials = reinterpret_cast<float*>(ws + w.parts);
     double* G = reinterpret_cast<double*>(ws + w.G);

@@ -150,9 +150,10 @@ class LscFunction(torch.autograd.Function):
 class ChainFunction(torch.autograd.Function):
     """Fused Signal2SH -> LSC -> SH2Signal on tcgen05 (dl_chain_fwd_f32 / dl_chain_bwd_f32).
 
-    Forward is one kernel (x -> y).  Backward is one kernel for dx (the adjoint chain) and
-    one Gram kernel for the LSC parameters (+ a float64 finalize).  The intermediates never
-    touch HBM; x is kept for the weight gradient.
+    Forward is one kernel (x -> y) that also writes the Signal2SH coefficients c = M x
+    (zero-padded rows, `c_mid`) for the weight gradient; x itself is not kept.  Backward is
+    one kernel for dx (the adjoint chain, which writes g = B'^T dy to `g_mid`), one Gram
+    kernel over (g_mid, c_mid) for the LSC parameters, and a float64 finalize.
     """
 
     @staticmethod
@@ -162,41 +163,49 @@ class ChainFunction(torch.autograd.Function):
         n = M.shape[-1]
         n_out = Bt.shape[0]
         B, V = x.shape[0], nvox_of(x)
+        lib = _lib.load()
+        want_w = ctx.needs_input_grad[1] or (bias is not None and ctx.needs_input_grad[2])
         L, _, bvec = build_lsc_operator(fold, beta, weight, bias, want_Lt=False)
         y = torch.empty((B, s_out * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
-        lib = _lib.load()
+        c_mid = (torch.empty((B, lib.dl_chain_mid_rows(s_in, r_in), V), dtype=torch.float32, device=x.device)
+                 if want_w else None)
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
-        _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt), _p(ws),
-                  B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
-        ctx.save_for_backward(x, weight, M, fold, beta, Bt, L)
+        _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(c_mid), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt),
+                  _p(ws), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
+        ctx.save_for_backward(c_mid, weight, M, fold, beta, Bt, L)
         ctx.per_shell = per_shell
         ctx.has_bias = bias is not None
+        ctx.shape = (B, V, tuple(x.shape))
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x, weight, M, fold, beta, Bt, L = ctx.saved_tensors
+        c_mid, weight, M, fold, beta, Bt, L = ctx.saved_tensors
         s_out, s_in = weight.shape[0], weight.shape[1]
         K, r_out, r_in = fold.shape
         n = M.shape[-1]
         n_out = Bt.shape[0]
-        B, V = x.shape[0], nvox_of(x)
+        B, V, xshape = ctx.shape
         dy = as_device_f32(dy, "grad")
         want_x = ctx.needs_input_grad[0]
-        want_w = ctx.needs_input_grad[1]
-        want_b = ctx.has_bias and ctx.needs_input_grad[2]
-        dx = torch.empty_like(x) if want_x else None
-        dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=x.device) if want_w else None
-        db = torch.empty((s_out,), dtype=torch.float32, device=x.device) if want_b else None
-        if dx is None and dW is None and db is None:
+        want_w = ctx.needs_input_grad[1] and c_mid is not None
+        want_b = ctx.has_bias and ctx.needs_input_grad[2] and c_mid is not None
+        if not (want_x or want_w or want_b):
             return None, None, None, None, None, None, None, None
         lib = _lib.load()
-        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
-        _lib.call("dl_chain_bwd_f32", _p(x), _p(dy), _p(dx), _p(dW), _p(db), _p(M), int(ctx.per_shell), _p(L),
-                  _p(Bt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out, n_out, V, _stream())
+        # the adjoint kernel always runs (it produces g for the Gram); dx is discarded if not wanted
+        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
+        dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=dy.device) if want_w else None
+        db = torch.empty((s_out,), dtype=torch.float32, device=dy.device) if want_b else None
+        g_mid = (torch.empty((B, lib.dl_chain_mid_rows(s_out, r_out), V), dtype=torch.float32, device=dy.device)
+                 if (want_w or want_b) else None)
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
+        _lib.call("dl_chain_bwd_f32", _p(c_mid), _p(dy), _p(dx), _p(dW), _p(db), _p(g_mid), _p(M),
+                  int(ctx.per_shell), _p(L), _p(Bt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out,
+                  n_out, V, _stream())
         if dW is not None:
             dW = dW.view(weight.shape)
-        return dx, dW, db, None, None, None, None, None
+        return (dx if want_x else None), dW, db, None, None, None, None, None
 
 
 def chain_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int, per_shell: bool) -> bool:
