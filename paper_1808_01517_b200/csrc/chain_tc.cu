@@ -44,7 +44,7 @@ constexpr int kThreads = (kWarpLD + 1) * 32;
 constexpr int kBoxV = kTileV + 4;           // TMA box width: 128 voxels + a 16-byte realignment margin
 constexpr int kStageBytes = 16 * kBoxV * 4; // one ring stage: 16 channels x 132 voxels fp32
 constexpr int kMaxSlots = 6;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;
 
 // ---------------------------------------------------------------------------- small helpers
 template <int P> struct Pairs;
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], kGMID);
+      mbar_init(&bars.empty[s], 1);   // each chunk is converted by one MID warp
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.tiles_full[b], kGMID);
@@ -983,60 +983,60 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
     const float* sbeta = reinterpret_cast<const float*>(smem + p.sm_beta);
     const int sh = (int)(p.nvox & 3);
     float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t s = 0, round = 0, it = 0;
+    uint32_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kGV;
       const uint32_t buf = it & 1;
       if (it >= 2) mbar_wait_warp(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
       uint8_t* tb = smem + p.sm_buf0 + buf * p.buf_bytes;
       const bool ok0 = v0 + 2 * lane < p.nvox, ok1 = v0 + 2 * lane + 1 < p.nvox;
-      for (int r = 0; r < per_tile; ++r) {
+      // this warp converts whole chunks r = warp, warp + 8, ... (16 rows x 64 voxels each)
+      for (int r = warp; r < per_tile; r += kGMID) {
         const bool isg = r < nG;
         const int row0 = 16 * (isg ? r : r - nG);
-        float x[2][2];   // two rows of this warp, two voxels of this lane
+        // ring position of chunk (it, r): chunks are numbered tile-major, kGMID warps share the ring
+        const uint32_t q = it * (uint32_t)per_tile + (uint32_t)r;
+        const uint32_t cs = q % NS, cround = q / NS;
+        float x[16][2];
         if (p.tma) {
-          mbar_wait_warp(&bars.full[s], round & 1);
-          const float* st = reinterpret_cast<const float*>(smem + p.sm_ring + s * kGStage);
+          mbar_wait_warp(&bars.full[cs], cround & 1);
+          const float* st = reinterpret_cast<const float*>(smem + p.sm_ring + cs * kGStage) + 2 * lane;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = 2 * warp + h;   // row within the chunk; even rows in box 0, odd in box 1
-            const float2 v2 = *reinterpret_cast<const float2*>(st + (j & 1) * (8 * kGBoxV + sh) + (j >> 1) * kGBoxV +
-                                                               2 * lane);
-            x[h][0] = ok0 ? v2.x : 0.f;
-            x[h][1] = ok1 ? v2.y : 0.f;
+          for (int j = 0; j < 16; ++j) {   // even rows in box 0, odd rows in box 1 (shifted by sh)
+            const float2 v2 = *reinterpret_cast<const float2*>(st + (j & 1) * (8 * kGBoxV + sh) + (j >> 1) * kGBoxV);
+            x[j][0] = ok0 ? v2.x : 0.f;
+            x[j][1] = ok1 ? v2.y : 0.f;
           }
-          warp_arrive(&bars.empty[s]);
-          if (++s == NS) {
-            s = 0;
-            ++round;
-          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars.empty[cs]);
         } else {
-          const float* src = isg ? p.g + b * p.g_bs : p.c + b * p.c_bs;
+          const float* src = (isg ? p.g + b * p.g_bs : p.c + b * p.c_bs) + (int64_t)row0 * p.nvox + v0 + 2 * lane;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float* rp = src + (int64_t)(row0 + 2 * warp + h) * p.nvox + v0 + 2 * lane;
-            x[h][0] = ok0 ? __ldg(rp) : 0.f;
-            x[h][1] = ok1 ? __ldg(rp + 1) : 0.f;
+          for (int j = 0; j < 16; ++j) {
+            x[j][0] = ok0 ? __ldg(src + (int64_t)j * p.nvox) : 0.f;
+            x[j][1] = ok1 ? __ldg(src + (int64_t)j * p.nvox + 1) : 0.f;
           }
         }
         uint8_t* part0 = tb + (isg ? 2 * p.cpart : 0);
         const uint32_t pstride = isg ? p.gpart : p.cpart;
+        const uint32_t lo4 = (uint32_t)(lane & 3) * 4u, ch = (uint32_t)(lane >> 2);
+        uint8_t* rb = part0 + (uint32_t)(row0 >> 3) * 1024u + lo4;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = row0 + 2 * warp + h;
-          const uint32_t hi = pack_bf16x2(x[h][0], x[h][1]);
-          const uint32_t lo = pack_bf16x2(x[h][0] - bf16lo_to_f32(hi), x[h][1] - bf16hi_to_f32(hi));
-          const uint32_t off = (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
-                               ((uint32_t)((lane >> 2) ^ (row & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
-          *reinterpret_cast<uint32_t*>(part0 + off) = hi;
-          *reinterpret_cast<uint32_t*>(part0 + pstride + off) = lo;
-          if (isg) {
-            const int o = row / p.RPo;
-            const float bt = sbeta[row - o * p.RPo] * (x[h][0] + x[h][1]);
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t hi = pack_bf16x2(x[j][0], x[j][1]);
+          const uint32_t lo = pack_bf16x2(x[j][0] - bf16lo_to_f32(hi), x[j][1] - bf16hi_to_f32(hi));
+          const uint32_t off = (uint32_t)(j >> 3) * 1024u + (uint32_t)(j & 7) * 128u + ((ch ^ (uint32_t)(j & 7)) << 4);
+          *reinterpret_cast<uint32_t*>(rb + off) = hi;
+          *reinterpret_cast<uint32_t*>(rb + pstride + off) = lo;
+        }
+        if (isg) {   // RPo % 16 == 0: the chunk lies in one output shell
+          const int o = row0 / p.RPo, rr = row0 - o * p.RPo;
+          float acc = 0.f;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (q == o) dbacc[q] += bt;
-          }
+          for (int j = 0; j < 16; ++j) acc += sbeta[rr + j] * (x[j][0] + x[j][1]);
+#pragma unroll
+          for (int qo = 0; qo < 4; ++qo)
+            if (qo == o) dbacc[qo] += acc;
         }
       }
       fence_proxy_async();   // generic-proxy tile writes -> visible to the tensor core
@@ -1368,7 +1368,8 @@ bool plan_chain3v(Chain3& p, int parts) {
   p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (p.ns = kMaxStages; p.ns >= 2; --p.ns) {
+  for (int ns : {12, 10, 8, 7, 6, 5, 4, 3, 2}) {
+    p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
     p.sm_bar = (uint32_t)q;
     q = al(q + sizeof(Bars3v), 16);
@@ -1396,7 +1397,8 @@ bool plan_gram(GramP& p) {
   p.sm_buf0 = (uint32_t)o; o = al(o + 2 * (size_t)p.buf_bytes + 8192, 1024);
   p.sm_beta = (uint32_t)o; o = al(o + (size_t)p.RPo * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (p.ns = kMaxStages; p.ns >= 2; --p.ns) {
+  for (int ns : {16, 12, 8, 6, 4, 2}) {
+    p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kGStage, 16);
     p.sm_bar = (uint32_t)q;
     q = al(q + sizeof(BarsG), 16);
@@ -1430,7 +1432,9 @@ int run_chain3v(const Chain3& p, int grid, cudaStream_t st) {
     case 5: return launch_chain3v<PARTS, 5>(p, grid, st);
     case 6: return launch_chain3v<PARTS, 6>(p, grid, st);
     case 7: return launch_chain3v<PARTS, 7>(p, grid, st);
-    default: return launch_chain3v<PARTS, 8>(p, grid, st);
+    case 8: return launch_chain3v<PARTS, 8>(p, grid, st);
+    case 10: return launch_chain3v<PARTS, 10>(p, grid, st);
+    default: return launch_chain3v<PARTS, 12>(p, grid, st);
   }
 }
 
@@ -1452,12 +1456,11 @@ int launch_gram(const GramP& p, int grid, cudaStream_t st) {
 int run_gram(const GramP& p, int grid, cudaStream_t st) {
   switch (p.ns) {
     case 2: return launch_gram<2>(p, grid, st);
-    case 3: return launch_gram<3>(p, grid, st);
     case 4: return launch_gram<4>(p, grid, st);
-    case 5: return launch_gram<5>(p, grid, st);
     case 6: return launch_gram<6>(p, grid, st);
-    case 7: return launch_gram<7>(p, grid, st);
-    default: return launch_gram<8>(p, grid, st);
+    case 8: return launch_gram<8>(p, grid, st);
+    case 12: return launch_gram<12>(p, grid, st);
+    default: return launch_gram<16>(p, grid, st);
   }
 }
 
