@@ -12,7 +12,8 @@ import threading
 
 from .errors import DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdelimit_sm100a.so")
+LIB_PATH = os.environ.get("DELIMIT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libdelimit_sm100a.so")
 
 _c_p = ctypes.c_void_p
 _i64 = ctypes.c_int64

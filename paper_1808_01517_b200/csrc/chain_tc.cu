@@ -45,6 +45,10 @@ constexpr int kBoxV = kTileV + 4;           // TMA box width: 128 voxels + a 16-
 constexpr int kStageBytes = 16 * kBoxV * 4; // one ring stage: 16 channels x 132 voxels fp32
 constexpr int kMaxSlots = 6;
 constexpr int kMaxStages = 16;
+#ifndef DL_HINT_NS
+#define DL_HINT_NS 1000
+#endif
+constexpr uint32_t kHintNs = DL_HINT_NS;   // suspend hint for long, latency-tolerant waits
 
 // ---------------------------------------------------------------------------- small helpers
 template <int P> struct Pairs;
@@ -94,6 +98,23 @@ __device__ __forceinline__ void split_store16(uint32_t taddr_part0, uint32_t par
 #pragma unroll
     for (int q = 0; q < PARTS; ++q) w[q][i] = pp[q];
   }
+#pragma unroll
+  for (int q = 0; q < PARTS; ++q) tmem_st<8>(taddr_part0 + (uint32_t)q * part_stride_cols, w[q]);
+}
+
+// split only (registers), so the TMEM slot can be awaited after the arithmetic
+template <int PARTS>
+__device__ __forceinline__ void split16(const float (&v)[16], uint32_t (&w)[PARTS][8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t pp[PARTS];
+    split_pair<PARTS>(v[2 * i], v[2 * i + 1], pp);
+#pragma unroll
+    for (int q = 0; q < PARTS; ++q) w[q][i] = pp[q];
+  }
+}
+template <int PARTS>
+__device__ __forceinline__ void store_parts(uint32_t taddr_part0, uint32_t part_stride_cols, const uint32_t (&w)[PARTS][8]) {
 #pragma unroll
   for (int q = 0; q < PARTS; ++q) tmem_st<8>(taddr_part0 + (uint32_t)q * part_stride_cols, w[q]);
 }
@@ -150,9 +171,11 @@ __device__ __forceinline__ void stream_chunk(float* dst, const float* src, int64
 template <int PARTS>
 __device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int NA, uint64_t* a_full,
                                       uint64_t* a_empty, uint32_t& aslot, uint32_t& around, int step = 1) {
+  uint32_t w[PARTS][8];
+  split16<PARTS>(v, w);
   if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
   fence_after();
-  split_store16<PARTS>(tslots + aslot * (PARTS * 8), 8, v);
+  store_parts<PARTS>(tslots + aslot * (PARTS * 8), 8, w);
   tmem_wait_st();
   fence_before();
   warp_arrive(&a_full[aslot]);
@@ -640,6 +663,7 @@ struct Bars3v {
 
 template <int PARTS, int NS>
 __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant__ Chain3 p) {
+  static_assert(NS % 2 == 0, "two IN warps alternate chunks: each ring stage needs one fixed consumer pair");
   extern __shared__ __align__(1024) uint8_t smem[];
   Bars3v& bars = *reinterpret_cast<Bars3v*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -745,9 +769,11 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #pragma unroll
           for (int e = 0; e < 16; ++e) v[e] += bb[e];
         }
+        uint32_t w[PARTS][8];
+        split16<PARTS>(v, w);
         if (cround > 0) mbar_wait_warp(&bars.c_empty[cslot], (cround - 1) & 1);
         fence_after();
-        split_store16<PARTS>(tq + p.colC + cslot * kSlotW, 8, v);
+        store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
         tmem_wait_st();
         fence_before();
         warp_arrive(&bars.c_full[cslot]);
@@ -770,7 +796,8 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
       for (int o = 0; o < p.G2; ++o, ++n3) {
-        mbar_wait_warp(&bars.d3_full, n3 & 1);
+        mbar_wait_hint(&bars.d3_full, n3 & 1, kHintNs);
+        __syncwarp();
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
         fence_after();
         for (int ck = cg; ck < p.N3 / 16; ck += 2) {
@@ -947,6 +974,7 @@ struct BarsG {
 
 template <int NS>
 __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ GramP p) {
+  static_assert(NS % kGMID == 0, "each ring stage needs one fixed consumer warp");
   extern __shared__ __align__(1024) uint8_t smem[];
   BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -990,12 +1018,15 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
       if (it >= 2) mbar_wait_warp(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
       uint8_t* tb = smem + p.sm_buf0 + buf * p.buf_bytes;
       const bool ok0 = v0 + 2 * lane < p.nvox, ok1 = v0 + 2 * lane + 1 < p.nvox;
-      // this warp converts whole chunks r = warp, warp + 8, ... (16 rows x 64 voxels each)
-      for (int r = warp; r < per_tile; r += kGMID) {
+      // chunk q (CTA-wide, tile-major) is converted by warp q % kGMID.  NS is a multiple of kGMID, so
+      // every ring stage has one fixed consumer that takes its rounds in order (a parity wait can
+      // never run a whole phase ahead of the stage).
+      const uint32_t q0 = it * (uint32_t)per_tile;
+      const int rfirst = (int)(((uint32_t)warp + kGMID - q0 % kGMID) % kGMID);
+      for (int r = rfirst; r < per_tile; r += kGMID) {
         const bool isg = r < nG;
         const int row0 = 16 * (isg ? r : r - nG);
-        // ring position of chunk (it, r): chunks are numbered tile-major, kGMID warps share the ring
-        const uint32_t q = it * (uint32_t)per_tile + (uint32_t)r;
+        const uint32_t q = q0 + (uint32_t)r;
         const uint32_t cs = q % NS, cround = q / NS;
         float x[16][2];
         if (p.tma) {
@@ -1368,7 +1399,8 @@ bool plan_chain3v(Chain3& p, int parts) {
   p.sm_w3 = (uint32_t)o; o = al(o + (size_t)parts * p.w3_groups * p.w3_img, 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (int ns : {12, 10, 8, 7, 6, 5, 4, 3, 2}) {
+  // even depths: two IN warps take alternate chunks, so each stage keeps one fixed consumer pair
+  for (int ns : {12, 10, 8, 6, 4, 2}) {
     p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
     p.sm_bar = (uint32_t)q;
@@ -1397,7 +1429,7 @@ bool plan_gram(GramP& p) {
   p.sm_buf0 = (uint32_t)o; o = al(o + 2 * (size_t)p.buf_bytes + 8192, 1024);
   p.sm_beta = (uint32_t)o; o = al(o + (size_t)p.RPo * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (int ns : {16, 12, 8, 6, 4, 2}) {
+  for (int ns : {16, 8}) {
     p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kGStage, 16);
     p.sm_bar = (uint32_t)q;
@@ -1427,11 +1459,8 @@ template <int PARTS>
 int run_chain3v(const Chain3& p, int grid, cudaStream_t st) {
   switch (p.ns) {
     case 2: return launch_chain3v<PARTS, 2>(p, grid, st);
-    case 3: return launch_chain3v<PARTS, 3>(p, grid, st);
     case 4: return launch_chain3v<PARTS, 4>(p, grid, st);
-    case 5: return launch_chain3v<PARTS, 5>(p, grid, st);
     case 6: return launch_chain3v<PARTS, 6>(p, grid, st);
-    case 7: return launch_chain3v<PARTS, 7>(p, grid, st);
     case 8: return launch_chain3v<PARTS, 8>(p, grid, st);
     case 10: return launch_chain3v<PARTS, 10>(p, grid, st);
     default: return launch_chain3v<PARTS, 12>(p, grid, st);
@@ -1455,11 +1484,7 @@ int launch_gram(const GramP& p, int grid, cudaStream_t st) {
 
 int run_gram(const GramP& p, int grid, cudaStream_t st) {
   switch (p.ns) {
-    case 2: return launch_gram<2>(p, grid, st);
-    case 4: return launch_gram<4>(p, grid, st);
-    case 6: return launch_gram<6>(p, grid, st);
     case 8: return launch_gram<8>(p, grid, st);
-    case 12: return launch_gram<12>(p, grid, st);
     default: return launch_gram<16>(p, grid, st);
   }
 }

@@ -307,6 +307,30 @@ def test_weight_grad_deterministic(dev, rng):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
+@pytest.mark.parametrize("nvox", [200_002, 200_001])
+def test_fused_chain_grads_bitwise_deterministic(dev, nvox):
+    """Fused fwd+bwd repeated on the same inputs gives bitwise-identical dx, dW, db: fixed work
+    partition, fixed-order float64 reduction, and no ring/barrier races (a stage read before its
+    TMA landed would show up here as run-to-run differences).  Odd nvox takes the cp.async path."""
+    d = unit_sphere_directions(90)
+    torch.manual_seed(3)
+    chain = dl.SphericalChain(dl.Signal2SH(8, d, lb_lambda=0.006).to(dev),
+                              dl.LocalSphericalConvolution(3, 3, 8, 8, d, [5]).to(dev), dl.SH2Signal(8, d).to(dev))
+    gen = torch.Generator(device=dev).manual_seed(5)
+    x = torch.rand((1, 270, nvox, 1, 1), generator=gen, device=dev).requires_grad_(True)
+    dy = torch.randn((1, 270, nvox, 1, 1), generator=gen, device=dev)
+    ref = None
+    for _ in range(12):
+        x.grad = None
+        chain.zero_grad(set_to_none=True)
+        chain(x).backward(dy)
+        got = (x.grad.clone(), chain.lsc.sconv.weight.grad.clone(), chain.lsc.sconv.bias.grad.clone())
+        if ref is None:
+            ref = got
+        else:
+            assert all(torch.equal(a, b) for a, b in zip(got, ref))
+
+
 def test_chain_cuda_graph_capture(golden, dev):
     s2sh, lsc, sh2s = chain_modules(golden, dev)
     chain = dl.SphericalChain(s2sh, lsc, sh2s)
