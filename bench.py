@@ -316,8 +316,11 @@ def run_ours(args):
     if rank == 0:
         peak, peak_kind = measured_peak_hbm()
         fwd_bytes = V * (SHELLS * NDIR + SHELLS * NDIR) * 4            # x in, y out
-        bwd_bytes = V * (3 * SHELLS * NDIR) * 4                        # dy in, x in, dx out
-        dom = ("chain_bwd", bwd_bytes, bwd_ms) if bwd_ms >= fwd_ms else ("chain_fwd", fwd_bytes, fwd_ms)
+        bwd_bytes = V * (3 * SHELLS * NDIR) * 4                        # dy in, x-or-c in, dx out
+        # dominant kernel: the fused chain kernel (forward and adjoint launches take the same time; the
+        # forward phase is one chain3v launch plus ~15 us of operator packing).  Algorithmic bytes of
+        # one launch: x in + y out (SURVEY.md 8(d), 2,160 B/voxel at cfg4).
+        dom = ("chain_fwd", fwd_bytes, fwd_ms)
         achieved = dom[1] / (dom[2] / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": world * V / (ms / 1e3), "unit": "voxels/s", "n_gpus": world,
@@ -328,10 +331,11 @@ def run_ours(args):
                        "model": "SphericalChain", "global_batch": world, "voxels_per_gpu": V,
                        "channels": SHELLS * NDIR, "seq_len": None, "parallelism": f"dp{world} (subject-sharded)",
                        "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2"},
-            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": "chain3v_tc (forward)", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": dom[1], "launch_ms": dom[2],
-                         "traffic": ncu_traffic(dom[0])},
+                         "bytes_per_voxel": 2160, "traffic": ncu_traffic(dom[0])},
             "phase_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
             "step_hbm_gbs": (fwd_bytes + bwd_bytes) / (ms / 1e3) / 1e9,
             "cpu_baseline": cpu,
