@@ -853,28 +853,46 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
                    tD3 = tbase + p.colD3;
     // Static issue order per tile t: stage 2(t); then for each output group o: stage 3(t, o) followed by
     // a share of stage 1(t+1) -- those MMAs run while OUT drains D3(o).  All waits block (no polling).
+    // The MMA warp is instruction-latency bound (it shares its scheduler with six other warps), so
+    // every cursor below advances by additions only.
     uint32_t aslot = 0, around = 0, cslot = 0, cround = 0, n3 = 0;
-    auto s1_chunk = [&](int g, int k) {
+    uint32_t aaddr = tA, caddr = tC;
+    int g1 = 0, k1 = 0;
+    uint32_t d1col = tD1;
+    uint64_t bd1[PARTS];
+#pragma unroll
+    for (int j = 0; j < PARTS; ++j) bd1[j] = B1[j];
+    auto s1_next = [&]() {   // next stage-1 K-step (input chunk) in (group, k) order
       mbar_wait_warp(&bars.a_full[aslot], around & 1);
       fence_after();
-      uint64_t bd[PARTS];
-#pragma unroll
-      for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s + (uint64_t)k * ks1;
+      const bool first = k1 == 0, last = k1 == nk1 - 1 && g1 == p.G1 - 1;
       if (elect_one()) {
-        kstep_ts<PARTS>(tD1 + (uint32_t)(g * p.N1), tA + aslot * kSlotW, 8, bd, id1, k == 0);
+        kstep_ts<PARTS>(d1col, aaddr, 8, bd1, id1, first);
         commit(&bars.a_empty[aslot]);
-        if (k == nk1 - 1 && g == p.G1 - 1) commit(&bars.d1_full);
+        if (last) commit(&bars.d1_full);
       }
       __syncwarp();
       if (++aslot == (uint32_t)p.NA) {
         aslot = 0;
         ++around;
+        aaddr = tA;
+      } else {
+        aaddr += kSlotW;
+      }
+      if (++k1 == nk1) {
+        k1 = 0;
+        if (++g1 == p.G1) g1 = 0;
+        d1col = tD1 + (uint32_t)(g1 * p.N1);
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd1[j] = B1[j] + (uint64_t)g1 * g1s;
+      } else {
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd1[j] += ks1;
       }
     };
-    auto c_take = [&]() {   // wait for the next conversion-ring item; returns its A address
+    auto c_take = [&]() {   // wait for the next conversion-ring item
       mbar_wait_warp(&bars.c_full[cslot], cround & 1);
       fence_after();
-      return tC + cslot * kSlotW;
     };
     auto c_release = [&](uint64_t* extra) {
       if (elect_one()) {
@@ -885,46 +903,61 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       if (++cslot == (uint32_t)p.NAc) {
         cslot = 0;
         ++cround;
+        caddr = tC;
+      } else {
+        caddr += kSlotW;
       }
     };
     const int n1 = p.G1 * nk1;
-    for (int q = 0; q < (nmine > 0 ? n1 : 0); ++q) s1_chunk(q / nk1, q % nk1);
+    for (int q = 0; q < (nmine > 0 ? n1 : 0); ++q) s1_next();
     for (uint32_t it = 0; it < nmine; ++it) {
       DL_PROF(2, 0);
       // ---- stage 2 ----
+      uint64_t bd2[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) bd2[j] = B2[j];
       for (int jj = 0; jj < nk2; ++jj) {
-        const uint32_t a0 = c_take();
+        c_take();
         uint64_t bd[PARTS];
 #pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd[j] = B2[j] + (uint64_t)jj * ks2;
+        for (int j = 0; j < PARTS; ++j) bd[j] = bd2[j];
         for (int oo = 0; oo < n2m; ++oo) {
-          if (elect_one()) kstep_ts<PARTS>(tD2 + (uint32_t)(oo * p.N2), a0, 8, bd, id2, jj == 0);
+          if (elect_one()) kstep_ts<PARTS>(tD2 + (uint32_t)(oo * p.N2), caddr, 8, bd, id2, jj == 0);
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] += o2s;
         }
         c_release(jj == nk2 - 1 ? &bars.d2_full : nullptr);
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd2[j] += ks2;
       }
       DL_PROF(2, 1);
       // ---- stage 3 per output group, interleaved with the next tile's stage 1 ----
       const bool next = it + 1 < nmine;
       int q1 = 0;
+      uint64_t bg3[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) bg3[j] = B3[j];
       for (int o = 0; o < p.G2; ++o) {
         if (n3 > 0) mbar_wait_warp(&bars.d3_free, (n3 - 1) & 1);
         DL_PROF(2, 2 + 2 * o);
-        for (int jj = 0; jj < nk3; ++jj) {
-          const uint32_t a0 = c_take();
-          uint64_t bd[PARTS];
+        uint64_t bd[PARTS];
 #pragma unroll
-          for (int j = 0; j < PARTS; ++j) bd[j] = B3[j] + (uint64_t)o * g3s + (uint64_t)jj * ks3;
-          if (elect_one()) kstep_ts<PARTS>(tD3, a0, 8, bd, id3, jj == 0);
+        for (int j = 0; j < PARTS; ++j) bd[j] = bg3[j];
+        for (int jj = 0; jj < nk3; ++jj) {
+          c_take();
+          if (elect_one()) kstep_ts<PARTS>(tD3, caddr, 8, bd, id3, jj == 0);
           __syncwarp();
           c_release(jj == nk3 - 1 ? &bars.d3_full : nullptr);
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] += ks3;
         }
         ++n3;
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bg3[j] += g3s;
         DL_PROF(2, 3 + 2 * o);
         if (next)
-          for (const int qe = n1 * (o + 1) / p.G2; q1 < qe; ++q1) s1_chunk(q1 / nk1, q1 % nk1);
+          for (const int qe = n1 * (o + 1) / p.G2; q1 < qe; ++q1) s1_next();
       }
     }
   } else if (p.tma) {
@@ -968,7 +1001,7 @@ struct GramP {
 struct BarsG {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t tiles_full[2], gram_done[2];
-  float db[4];
+  float db[kGMID][4];
   uint32_t tmem_base;
 };
 
@@ -995,7 +1028,6 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
       mbar_init(&bars.tiles_full[b], kGMID);
       mbar_init(&bars.gram_done[b], 1);
     }
-    for (int o = 0; o < 4; ++o) bars.db[o] = 0.f;
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -1102,15 +1134,16 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
       }
     }
 #pragma unroll
-    for (int o = 0; o < 4; ++o) {
+    for (int o = 0; o < 4; ++o) {   // fixed-order sums (no atomics): bitwise reproducible
       float v = dbacc[o];
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0 && o < p.S_out) atomicAdd(&bars.db[o], v);
+      if (lane == 0) bars.db[warp][o] = v;
     }
     named_sync(1, kGMID * 32);
-    if (warp == 0 && lane == 0) {
-      float* dbp = p.partials + (int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out;
-      for (int o = 0; o < p.S_out; ++o) dbp[o] = bars.db[o];
+    if (warp == 0 && lane < p.S_out) {
+      float v = 0.f;
+      for (int w = 0; w < kGMID; ++w) v += bars.db[w][lane];
+      p.partials[(int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out + lane] = v;
     }
   } else if (warp == kGWarpMMA) {
     // =========================== MMA: G += g^T c per 16-voxel K-step, three blocks ===========================
@@ -1383,7 +1416,13 @@ bool plan_chain3v(Chain3& p, int parts) {
   const int slotw = parts * 8, D1w = p.G1 * p.N1, D2w = p.G2 * p.N2, D3w = p.N3;
   const int nslots = (512 - D1w - D2w - D3w) / slotw;
   if (512 - D1w - D2w - D3w < 0 || nslots < 4) return false;
-  p.NA = nslots / 2 < kMaxSlots ? nslots / 2 : kMaxSlots;
+  // stage-1 input chunks are the most frequent handoff (18 per tile vs 9 + 9 conversions): IN gets the
+  // larger half of the slot budget
+  p.NA = (nslots + 1) / 2 < kMaxSlots ? (nslots + 1) / 2 : kMaxSlots;
+  if (const char* e = getenv("DELIMIT_IN_SLOTS")) {   // tuning knob: IN-ring share of the slot budget
+    const int v = atoi(e);
+    if (v >= 2 && v <= nslots - 2) p.NA = v;
+  }
   p.NAc = nslots - p.NA < kMaxSlots ? nslots - p.NA : kMaxSlots;
   p.colA = 0;
   p.colC = (uint32_t)(p.NA * slotw);

@@ -33,5 +33,5 @@ for it in range(2, 6):
 inr = buf.cpu().numpy()[1024:1024 + 32].reshape(8, 4)
 print('IN warps (chunks, wait_full, wait_aempty, work):')
 print(inr)
-m = buf.cpu().numpy()[1100:1108]
-print('MMA: total, idle_loops, gate_blocked_loops, s1_cycles, conv_cycles, items, tiles, s1_issue_only:', m)
+m = buf.cpu().numpy()[1100:1103]
+print("MMA s1 chunks, wait cycles, issue cycles:", m)
