@@ -45,10 +45,10 @@ constexpr int kBoxV = kTileV + 4;           // TMA box width: 128 voxels + a 16-
 constexpr int kStageBytes = 16 * kBoxV * 4; // one ring stage: 16 channels x 132 voxels fp32
 constexpr int kMaxSlots = 6;
 constexpr int kMaxStages = 16;
-#ifndef DL_HINT_NS
-#define DL_HINT_NS 1000
+#ifndef DL_SLEEP_NS
+#define DL_SLEEP_NS 0
 #endif
-constexpr uint32_t kHintNs = DL_HINT_NS;   // suspend hint for long, latency-tolerant waits
+constexpr uint32_t kSleepNs = DL_SLEEP_NS;   // back-off between polls of non-MMA roles (0 = spin)
 
 // ---------------------------------------------------------------------------- small helpers
 template <int P> struct Pairs;
@@ -141,6 +141,12 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
+// wait used by the IN / CONV / OUT / loader roles (the MMA warp keeps mbar_wait_warp)
+__device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) {
+  if (kSleepNs) mbar_wait_sleep(bar, parity, kSleepNs);
+  else mbar_wait_warp(bar, parity);
+}
+
 // byte offset of (row j, voxel k) in a SWIZZLE_128B K-major tile with `rows` rows (K = 128 voxels)
 __device__ __forceinline__ uint32_t sw128_off(int j, int k, int rows) {
   return (uint32_t)(k >> 6) * (uint32_t)(rows >> 3) * 1024u + (uint32_t)(j >> 3) * 1024u + (uint32_t)(j & 7) * 128u +
@@ -173,7 +179,7 @@ __device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int
                                       uint64_t* a_empty, uint32_t& aslot, uint32_t& around, int step = 1) {
   uint32_t w[PARTS][8];
   split16<PARTS>(v, w);
-  if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
+  if (around > 0) role_wait(&a_empty[aslot], (around - 1) & 1);
   fence_after();
   store_parts<PARTS>(tslots + aslot * (PARTS * 8), 8, w);
   tmem_wait_st();
@@ -254,7 +260,7 @@ __device__ __forceinline__ void tma_loader(const Geo& geo, int per_tile, int64_t
     const int v0 = (int)((t - b * tiles_per_b) * kTileV);
     for (int r = 0; r < per_tile; ++r) {
       const ChunkGeo cg = geo(r);
-      if (round > 0) mbar_wait_warp(&empty[s], (round - 1) & 1);
+      if (round > 0) role_wait(&empty[s], (round - 1) & 1);
       if (elect_one()) {
         uint8_t* dst = ring + s * kStageBytes;
         mbar_arrive_tx(&full[s], kStageBytes);
@@ -277,8 +283,7 @@ template <int PARTS, int NS, typename Geo>
 __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                             int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
                                             const float* ring, uint64_t* full, uint64_t* empty, int iw = 0,
-                                            int nIW = 1, long long* prof = nullptr) {
-  long long tw_full = 0, tw_empty = 0, tw_split = 0, n_ch = 0;
+                                            int nIW = 1) {
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int odd0 = 8 * kBoxV + (int)(nvox & 3);   // first odd-channel value of this thread, minus its voxel
   uint32_t s = 0, round = 0, aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
@@ -296,31 +301,14 @@ __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_
       if ((q & (uint32_t)(nIW - 1)) != (uint32_t)iw) continue;
       const ChunkGeo cg = geo(r);
       const int nval = vok ? cg.nval : 0;   // voxels past nvox read neighbouring-row data: zero them
-      long long c0 = clock64();
-      mbar_wait_warp(&full[cs], cround & 1);
-      long long c1 = clock64();
+      role_wait(&full[cs], cround & 1);
       const float* rp = ring + cs * (kStageBytes / 4) + 32 * qd + lane;
       float v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = j < nval ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
       warp_arrive(&empty[cs]);
-      long long c2 = clock64();
-      if (around > 0) mbar_wait_warp(&a_empty[aslot], (around - 1) & 1);
-      long long c3 = clock64();
       put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
-      long long c4 = clock64();
-      tw_full += c1 - c0;
-      tw_empty += c3 - c2;
-      tw_split += c4 - c3 + c2 - c1;
-      ++n_ch;
     }
-  }
-  if (prof && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
-    const int w = threadIdx.x >> 5;
-    prof[1024 + 4 * w + 0] = n_ch;
-    prof[1024 + 4 * w + 1] = tw_full;
-    prof[1024 + 4 * w + 2] = tw_empty;
-    prof[1024 + 4 * w + 3] = tw_split;
   }
 }
 
@@ -723,8 +711,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
     if (p.tma) {
       in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
-                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty, warp >> 2, 2,
-                             p.prof);
+                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty, warp >> 2, 2);
     } else if (warp < 4) {
       const float* const base[2] = {p.in, p.in};
       const int64_t bs[2] = {p.in_bs, p.in_bs};
@@ -745,7 +732,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       const int64_t b = t / p.tiles_per_b, vx = (t - b * p.tiles_per_b) * kTileV + 32 * (warp & 3) + lane;
       const bool vok = vx < p.nvox;
       if (warp == kIN3) DL_PROF(1, 0);
-      mbar_wait_warp(&bars.d1_full, it & 1);
+      role_wait(&bars.d1_full, it & 1);
       if (warp == kIN3) DL_PROF(1, 1);
       fence_after();
       bool d2_seen = false;
@@ -758,7 +745,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         } else {
           if (!d2_seen) {
             if (warp == kIN3) DL_PROF(1, 2);
-            mbar_wait_warp(&bars.d2_full, it & 1);
+            role_wait(&bars.d2_full, it & 1);
             if (warp == kIN3) DL_PROF(1, 3);
             fence_after();
             d2_seen = true;
@@ -771,7 +758,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         }
         uint32_t w[PARTS][8];
         split16<PARTS>(v, w);
-        if (cround > 0) mbar_wait_warp(&bars.c_empty[cslot], (cround - 1) & 1);
+        if (cround > 0) role_wait(&bars.c_empty[cslot], (cround - 1) & 1);
         fence_after();
         store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
         tmem_wait_st();
@@ -796,8 +783,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
       for (int o = 0; o < p.G2; ++o, ++n3) {
-        mbar_wait_hint(&bars.d3_full, n3 & 1, kHintNs);
-        __syncwarp();
+        role_wait(&bars.d3_full, n3 & 1);
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
         fence_after();
         for (int ck = cg; ck < p.N3 / 16; ck += 2) {
@@ -1047,7 +1033,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kGV;
       const uint32_t buf = it & 1;
-      if (it >= 2) mbar_wait_warp(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
+      if (it >= 2) role_wait(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
       uint8_t* tb = smem + p.sm_buf0 + buf * p.buf_bytes;
       const bool ok0 = v0 + 2 * lane < p.nvox, ok1 = v0 + 2 * lane + 1 < p.nvox;
       // chunk q (CTA-wide, tile-major) is converted by warp q % kGMID.  NS is a multiple of kGMID, so
@@ -1062,7 +1048,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
         const uint32_t cs = q % NS, cround = q / NS;
         float x[16][2];
         if (p.tma) {
-          mbar_wait_warp(&bars.full[cs], cround & 1);
+          role_wait(&bars.full[cs], cround & 1);
           const float* st = reinterpret_cast<const float*>(smem + p.sm_ring + cs * kGStage) + 2 * lane;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {   // even rows in box 0, odd rows in box 1 (shifted by sh)
@@ -1191,7 +1177,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
       const int v0 = (int)((t - b * p.tiles_per_b) * kGV);
       for (int r = 0; r < per_tile; ++r) {
         const int tensor = r < nG ? 0 : 1, j0 = 8 * (r < nG ? r : r - nG);
-        if (round > 0) mbar_wait_warp(&bars.empty[s], (round - 1) & 1);
+        if (round > 0) role_wait(&bars.empty[s], (round - 1) & 1);
         if (elect_one()) {
           uint8_t* dst = smem + p.sm_ring + s * kGStage;
           mbar_arrive_tx(&bars.full[s], kGStage);

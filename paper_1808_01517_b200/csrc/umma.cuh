@@ -178,18 +178,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Same, with a suspend-time hint (ns) for waits expected to be long: the warp parks instead of
-// re-polling, leaving issue slots to the other warps of its scheduler.
-__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(hint_ns)
-      : "memory");
-}
-
 // mbar_wait by a whole warp, reconverged afterwards (lanes leave the polling loop independently, and
 // the .sync.aligned tcgen05 ops / elect.sync that follow need the full warp).
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
@@ -247,6 +235,13 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+
+// Whole-warp wait that backs off with __nanosleep between polls: for producer/consumer roles whose
+// waits are long, so that parked warps stop taking issue slots from the ones doing work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+  __syncwarp();
 }
 
 // mbar_test by a converged warp, lane 0's answer broadcast (every lane takes the same branch).

@@ -30,8 +30,3 @@ t0 = min(v for v in b[2].ravel() if v)
 for it in range(2, 6):
     ev = sorted((int(b[it, r, e]) - t0, r, e) for r in range(4) for e in range(32) if b[it, r, e])
     print(f'tile {it}: ' + ' '.join(f'{r}.{e}@{t}' for t, r, e in ev))
-inr = buf.cpu().numpy()[1024:1024 + 32].reshape(8, 4)
-print('IN warps (chunks, wait_full, wait_aempty, work):')
-print(inr)
-m = buf.cpu().numpy()[1100:1103]
-print("MMA s1 chunks, wait cycles, issue cycles:", m)
