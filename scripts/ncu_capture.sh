@@ -6,6 +6,6 @@ tag=${1:-run}
 mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-clocks"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv $B > gpurun_out/${tag}_ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:chain3_tc -c 2 -f -o gpurun_out/${tag}_chain3 $B > gpurun_out/${tag}_ncu_chain3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:chain3 -c 2 -f -o gpurun_out/${tag}_chain3 $B > gpurun_out/${tag}_ncu_chain3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gram_tc -c 1 -f -o gpurun_out/${tag}_gram $B > gpurun_out/${tag}_ncu_gram.log 2>&1
 echo done
