@@ -636,7 +636,14 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
 // Ordering facts that replace explicit "free" barriers: CONV reads D1(t) only in the stage-2 items of
 // tile t and D2(t-1) only before the first stage-2 item of tile t, so the MMA may overwrite D1 once it
 // has consumed stage-2 item nk2-1 of tile t, and D2 once it consumes stage-2 item 0 of tile t+1.
-constexpr int kIN3 = 8, kCV3 = 8, kOUT3 = 8;
+#ifndef DL_CV_PER_Q
+#define DL_CV_PER_Q 2
+#endif
+#ifndef DL_OUT_PER_Q
+#define DL_OUT_PER_Q 2
+#endif
+constexpr int kCVQ = DL_CV_PER_Q, kOUTQ = DL_OUT_PER_Q;   // CONV / OUT warps per TMEM lane quadrant
+constexpr int kIN3 = 8, kCV3 = 4 * kCVQ, kOUT3 = 4 * kOUTQ;
 constexpr int kW3MMA = kIN3 + kCV3 + kOUT3;   // 24
 constexpr int kW3LD = kW3MMA + 1;             // 25
 constexpr int kThreads3 = (kW3LD + 1) * 32;
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
   } else if (warp < kIN3 + kCV3) {
     // =========================== CONV: accumulators -> conversion ring ===========================
     // items per tile: nk2 D1 chunks (stage-2 A), then G2 x nk3 D2 chunks (+bias, stage-3 A); this warp
-    // converts items i = cw, cw + 2, ... of the CTA-wide sequence (slot i % NAc)
+    // converts items i = cw, cw + kCVQ, ... of the CTA-wide sequence (slot i % NAc)
     const int cw = (warp - kIN3) >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
     const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
@@ -737,7 +744,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       fence_after();
       bool d2_seen = false;
       int i = i0;
-      for (; i < per_c; i += 2) {
+      for (; i < per_c; i += kCVQ) {
         float v[16];
         if (i < nk2) {
           ld16f(tq + p.colD1 + (uint32_t)i * 16, v);
@@ -764,7 +771,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         tmem_wait_st();
         fence_before();
         warp_arrive(&bars.c_full[cslot]);
-        cslot += 2;
+        cslot += kCVQ;
         while (cslot >= (uint32_t)p.NAc) {
           cslot -= p.NAc;
           ++cround;
@@ -786,7 +793,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         role_wait(&bars.d3_full, n3 & 1);
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
         fence_after();
-        for (int ck = cg; ck < p.N3 / 16; ck += 2) {
+        for (int ck = cg; ck < p.N3 / 16; ck += kOUTQ) {
           float vv[16];
           ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
           if (vok) {
@@ -1410,6 +1417,11 @@ bool plan_chain3v(Chain3& p, int parts) {
     if (v >= 2 && v <= nslots - 2) p.NA = v;
   }
   p.NAc = nslots - p.NA < kMaxSlots ? nslots - p.NA : kMaxSlots;
+  if (p.NAc < kCVQ) {   // kCVQ CONV warps alternate items: the ring needs >= kCVQ slots (parity safety)
+    p.NAc = kCVQ;
+    p.NA = nslots - kCVQ;
+  }
+  if (p.NA < 2) return false;
   p.colA = 0;
   p.colC = (uint32_t)(p.NA * slotw);
   p.colD1 = p.colC + (uint32_t)(p.NAc * slotw);
