@@ -97,29 +97,30 @@ int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float
  *   L:  (s_out*r_out) x (s_in*r_in) folded LSC operator, bvec its bias response
  *       (dl_lsc_build_operator_f32); Bt: n_out x r_out SH basis at the output directions.
  * Forward: x (nbatch, s_in*n, nvox) -> y (nbatch, s_out*n_out, nvox) in one kernel.  If c_mid
- * is not NULL the Signal2SH coefficients c = M x are also written there, as
- * (nbatch, dl_chain_mid_rows(s_in, r_in), nvox) fp32 with each shell's r_in rows padded to a
- * multiple of 16 by exact zeros; the backward's weight gradient needs them.
+ * is not NULL the Signal2SH coefficients c = M x are also written there, as the backward's Gram
+ * operand: an opaque buffer of dl_chain_mid_bytes(nbatch, s_in, r_in, nvox) bytes (16-byte aligned)
+ * holding c's first two bf16 split terms per element (rows padded per shell to 16, voxels to 64).
  * Every product is an fp32-accurate split product (each fp32 operand as
  * DELIMIT_SPLIT_TERMS = 3 (default) or 2 bf16 terms, fp32 accumulation).
- * Backward: dy -> dx with the adjoint chain kernel (which also writes g = B'^T dy to g_mid,
- * (nbatch, dl_chain_mid_rows(s_out, r_out), nvox), when dW or db is requested); then the LSC
- * parameter gradient dW (s_out, s_in, K), db (s_out) from a Gram kernel over (g_mid, c_mid)
- * plus a float64 finalize.  dW / db may be NULL (then c_mid, g_mid, P, beta may be NULL).
+ * Backward: dy -> dx with the adjoint chain kernel, which also writes g = B'^T dy to g_mid
+ * (dl_chain_mid_bytes(nbatch, s_out, r_out, nvox) bytes) when dW or db is requested; then the LSC
+ * parameter gradient dW (s_out, s_in, K), db (s_out) from a streaming Gram kernel over
+ * (g_mid, c_mid) plus a float64 finalize.  dW / db may be NULL (then c_mid, g_mid, P, beta may be
+ * NULL).  dx must not be NULL.
  * workspace: dl_chain_workspace_bytes() bytes.  dl_chain_supported() says whether the
  * channel counts fit the kernels' TMEM/shared-memory plan (3 shells x order 8 x 90 dirs do).
  */
 int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
                        int m_per_shell);
 int dl_chain_split_terms(void);
-int64_t dl_chain_mid_rows(int64_t shells, int64_t r);
+size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvox);
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);
-int dl_chain_fwd_f32(const float* x, float* y, float* c_mid, const float* M, int m_per_shell, const float* L,
+int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
                      const float* bvec, const float* Bt, void* workspace, int64_t nbatch, int64_t s_in,
                      int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox,
                      void* stream);
-int dl_chain_bwd_f32(const float* c_mid, const float* dy, float* dx, float* dW, float* db, float* g_mid,
+int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
                      const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
                      const float* beta, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K,
                      int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);

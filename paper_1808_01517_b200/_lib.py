@@ -34,7 +34,7 @@ SIGNATURES = {
                                 _i64, _i64, _i64, _c_p]),
     "dl_chain_supported": (_int, [_i64] * 6 + [_int]),
     "dl_chain_split_terms": (_int, []),
-    "dl_chain_mid_rows": (_i64, [_i64, _i64]),
+    "dl_chain_mid_bytes": (_size, [_i64] * 4),
     "dl_chain_workspace_bytes": (_size, [_i64] * 8),
     "dl_chain_fwd_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p, _c_p] + [_i64] * 8 + [_c_p]),
     "dl_chain_bwd_f32": (_int, [_c_p] * 7 + [_int] + [_c_p] * 5 + [_i64] * 9 + [_c_p]),

@@ -136,6 +136,27 @@ __device__ __forceinline__ void store16(float* d, int64_t stride, const float (&
   }
 }
 
+__device__ __forceinline__ void st_cs_u16(uint16_t* p, uint32_t v) {
+  asm volatile("st.global.cs.u16 [%0], %1;\n" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
+
+// 16 D1 rows of one voxel as their first two bf16 split terms (w0 = hi, w1 = next term, packed row pairs)
+// -> the two term planes of the mid buffer (`plane` halfs apart, rows `pitch` apart).  Row `ones` (or -1)
+// is stored as exactly 1.0: a zero-weight padding row whose Gram column sums g (the bias gradient).
+__device__ __forceinline__ void store_mid(uint16_t* d, int64_t plane, int64_t pitch, const uint32_t (&w0)[8],
+                                          const uint32_t (&w1)[8], int ones) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t a = w0[i], c = w1[i];
+    if (2 * i == ones) { a = (a & 0xFFFF0000u) | 0x3F80u; c &= 0xFFFF0000u; }
+    if (2 * i + 1 == ones) { a = (a & 0x0000FFFFu) | 0x3F800000u; c &= 0x0000FFFFu; }
+    st_cs_u16(d + (int64_t)(2 * i) * pitch, a & 0xFFFFu);
+    st_cs_u16(d + (int64_t)(2 * i + 1) * pitch, a >> 16);
+    st_cs_u16(d + plane + (int64_t)(2 * i) * pitch, c & 0xFFFFu);
+    st_cs_u16(d + plane + (int64_t)(2 * i + 1) * pitch, c >> 16);
+  }
+}
+
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
@@ -317,7 +338,10 @@ struct Chain3 {
   CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
   const float* in;
   float* out;
-  float* mid;                         // optional: stage-1 accumulator D1 (G1*N1 padded rows) -> HBM
+  uint16_t* mid;                      // optional: stage-1 accumulator D1 -> HBM as two bf16 term planes,
+                                      // tiled [b][64-voxel tile][term][row][64] (one contiguous Gram tile)
+  int64_t mid_pitch;                  // voxels per mid row (nvox rounded up to 64)
+  int mid_ones;                       // D1 row stored as 1.0 (a padding row; the Gram's bias column) or -1
   const float* bias2;                 // real stage-2 bias per (group, channel < C2) or null
   const uint16_t* w1;                 // images, part-major: (q * groups + g) * img_bytes
   const uint16_t* w2;
@@ -441,8 +465,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
       for (int ck = cg; ck < D1w / 16; ck += 2) {
         float vv[16];
         ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
-        if (p.mid && vok) store16(p.mid + b * p.mid_bs + (int64_t)ck * 16 * stride + v, stride, vv);
-        split_store16<PARTS>(tq + p.colA2 + (uint32_t)ck * 8, D1w / 2, vv);
+        uint32_t w[PARTS][8];
+        split16<PARTS>(vv, w);
+        if (p.mid && v < p.mid_pitch)
+          store_mid(p.mid + ((b * (p.mid_pitch >> 6) + (v >> 6)) * 2 * D1w + 16 * ck) * 64 + (v & 63),
+                    (int64_t)D1w * 64, 64, w[0], w[1], vok ? p.mid_ones - 16 * ck : -1);
+        store_parts<PARTS>(tq + p.colA2 + (uint32_t)ck * 8, D1w / 2, w);
       }
       tmem_wait_st();
       fence_before();
@@ -748,7 +776,6 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         float v[16];
         if (i < nk2) {
           ld16f(tq + p.colD1 + (uint32_t)i * 16, v);
-          if (p.mid && vok) store16(p.mid + b * p.mid_bs + (int64_t)i * 16 * p.nvox + vx, p.nvox, v);
         } else {
           if (!d2_seen) {
             if (warp == kIN3) DL_PROF(1, 2);
@@ -765,6 +792,9 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         }
         uint32_t w[PARTS][8];
         split16<PARTS>(v, w);
+        if (i < nk2 && p.mid && vx < p.mid_pitch)
+          store_mid(p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2 + 16 * i) * 64 + (vx & 63), (int64_t)K2 * 64,
+                    64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
         if (cround > 0) role_wait(&bars.c_empty[cslot], (cround - 1) & 1);
         fence_after();
         store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
@@ -962,65 +992,53 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 }
 
 // ============================================================================ LSC weight Gram
-// G[j][i] = sum_v g_v[j] c_v[i] over this CTA's voxels, where c = M x (saved by the forward as its
-// stage-1 accumulator) and g = B'^T dy (written by the adjoint chain kernel the same way); both are
-// fp32 (B, rows, V) tensors with per-shell rows padded to 16 (padding rows are exact zeros).
-// 64-voxel tiles: a TMA ring streams 16-row x 68-voxel blocks; eight MID warps split each value into
-// two bf16 terms and write SWIZZLE_128B K-major operand tiles (row = channel, K = voxel), double
-// buffered, so the MMA warp's Gram of tile t overlaps the conversion of tile t+1.  The bias gradient
-// db[o] = sum_v beta . g_v[o] is summed from the fp32 values on the way.
-constexpr int kGV = 64;                         // voxels per Gram tile (one 128-byte K atom of bf16)
-constexpr int kGBoxV = kGV + 4;                 // TMA box width (16-byte realignment margin)
-constexpr int kGStage = 16 * kGBoxV * 4;        // ring stage: 16 rows x 68 voxels fp32
-constexpr int kGMID = 8;
-constexpr int kGWarpMMA = kGMID;
-constexpr int kGWarpLD = kGMID + 1;
+// G[j][i] = sum_v g_v[j] c_v[i] over this CTA's voxels.  c = M x is written by the forward chain kernel
+// and g = B'^T dy by the adjoint, both as two-term bf16 planes (hi, next term) with rows padded per shell
+// to 16 and voxels padded to 64 (zeros).  Those planes are exactly the operands: a TMA ring streams one
+// 64-voxel tile (c hi | c lo | g hi | g lo, SWIZZLE_128B K-major: row = channel, K = voxel) per stage and
+// the MMA warp accumulates the three split products in TMEM for the whole CTA -- no conversion warps.
+// c's first padding row holds 1.0, so G's column `ones` is sum_v g_v: the bias gradient comes out of
+// the same MMAs.  Epilogue: 4 warps read G once.
+constexpr int kGV = 64;                  // voxels per Gram tile (one 128-byte bf16 K atom)
+constexpr int kGEpi = 4;                 // epilogue warps (one per TMEM lane quadrant)
+constexpr int kGWarpMMA = kGEpi;
+constexpr int kGWarpLD = kGEpi + 1;
 constexpr int kGThreads = (kGWarpLD + 1) * 32;
 
 struct GramP {
-  CUtensorMap tm[2];         // channel-pair views of g (0) and c (1)
-  const float* g;
-  const float* c;
-  const float* beta;         // R_out
-  float* partials;           // [grid][GR*GC] then db [grid][S_out]
-  int64_t nbatch, nvox, g_bs, c_bs, tiles_per_b;
-  int GR, GC, S_out, RPo, R_out;
-  int tma, ns;
-  uint32_t sm_buf0, buf_bytes, cpart, gpart;   // buffer b at sm_buf0 + b*buf_bytes: c part0|c part1|g part0|g part1
-  uint32_t sm_beta, sm_ring, sm_bar, smem_bytes;
+  CUtensorMap tm[2];         // bf16 term planes of g (0) and c (1): dims (pitch, rows, 2 terms, nbatch)
+  float* partials;           // [grid][GR*GC]
+  int64_t nbatch, tiles_per_b;
+  int GR, GC;
+  int ns;
+  uint32_t cpart, gpart, stage_bytes;   // stage: c hi | c lo | g hi | g lo
+  uint32_t sm_ring, sm_bar, smem_bytes;
   uint32_t colGA, colGB, colGC;
 };
 
 struct BarsG {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t tiles_full[2], gram_done[2];
-  float db[kGMID][4];
+  uint64_t done;
   uint32_t tmem_base;
 };
 
 template <int NS>
 __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ GramP p) {
-  static_assert(NS % kGMID == 0, "each ring stage needs one fixed consumer warp");
   extern __shared__ __align__(1024) uint8_t smem[];
   BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
-    // operand tiles start zeroed: g rows GR..127 (block A's M padding) are never written
-    uint4* z = reinterpret_cast<uint4*>(smem + p.sm_buf0);
-    for (uint32_t i = threadIdx.x; i < 2 * p.buf_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    float* sb = reinterpret_cast<float*>(smem + p.sm_beta);
-    for (int i = threadIdx.x; i < p.RPo; i += blockDim.x) sb[i] = i < p.R_out ? __ldg(p.beta + i) : 0.f;
+    // g rows GR..127 (block A's M padding) are never loaded: zero them once in every stage
+    uint4* z = reinterpret_cast<uint4*>(smem + p.sm_ring);
+    for (uint32_t i = threadIdx.x; i < NS * p.stage_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
   if (warp == kGWarpMMA) tmem_alloc(&bars.tmem_base, 256);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], 1);   // each chunk is converted by one MID warp
+      mbar_init(&bars.empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars.tiles_full[b], kGMID);
-      mbar_init(&bars.gram_done[b], 1);
-    }
+    mbar_init(&bars.done, 1);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -1029,125 +1047,41 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
   fence_after();
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
-  const int nG = p.GR / 16, nC = p.GC / 16, per_tile = nG + nC;
 
-  if (warp < kGMID) {
-    // =========================== MID: fp32 rows -> two-term bf16 SW128 tiles ===========================
-    const float* sbeta = reinterpret_cast<const float*>(smem + p.sm_beta);
-    const int sh = (int)(p.nvox & 3);
-    float dbacc[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int64_t b = t / p.tiles_per_b, v0 = (t - b * p.tiles_per_b) * kGV;
-      const uint32_t buf = it & 1;
-      if (it >= 2) role_wait(&bars.gram_done[buf], ((it >> 1) - 1) & 1);   // Gram of tile it-2 done
-      uint8_t* tb = smem + p.sm_buf0 + buf * p.buf_bytes;
-      const bool ok0 = v0 + 2 * lane < p.nvox, ok1 = v0 + 2 * lane + 1 < p.nvox;
-      // chunk q (CTA-wide, tile-major) is converted by warp q % kGMID.  NS is a multiple of kGMID, so
-      // every ring stage has one fixed consumer that takes its rounds in order (a parity wait can
-      // never run a whole phase ahead of the stage).
-      const uint32_t q0 = it * (uint32_t)per_tile;
-      const int rfirst = (int)(((uint32_t)warp + kGMID - q0 % kGMID) % kGMID);
-      for (int r = rfirst; r < per_tile; r += kGMID) {
-        const bool isg = r < nG;
-        const int row0 = 16 * (isg ? r : r - nG);
-        const uint32_t q = q0 + (uint32_t)r;
-        const uint32_t cs = q % NS, cround = q / NS;
-        float x[16][2];
-        if (p.tma) {
-          role_wait(&bars.full[cs], cround & 1);
-          const float* st = reinterpret_cast<const float*>(smem + p.sm_ring + cs * kGStage) + 2 * lane;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {   // even rows in box 0, odd rows in box 1 (shifted by sh)
-            const float2 v2 = *reinterpret_cast<const float2*>(st + (j & 1) * (8 * kGBoxV + sh) + (j >> 1) * kGBoxV);
-            x[j][0] = ok0 ? v2.x : 0.f;
-            x[j][1] = ok1 ? v2.y : 0.f;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars.empty[cs]);
-        } else {
-          const float* src = (isg ? p.g + b * p.g_bs : p.c + b * p.c_bs) + (int64_t)row0 * p.nvox + v0 + 2 * lane;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            x[j][0] = ok0 ? __ldg(src + (int64_t)j * p.nvox) : 0.f;
-            x[j][1] = ok1 ? __ldg(src + (int64_t)j * p.nvox + 1) : 0.f;
-          }
-        }
-        uint8_t* part0 = tb + (isg ? 2 * p.cpart : 0);
-        const uint32_t pstride = isg ? p.gpart : p.cpart;
-        const uint32_t lo4 = (uint32_t)(lane & 3) * 4u, ch = (uint32_t)(lane >> 2);
-        uint8_t* rb = part0 + (uint32_t)(row0 >> 3) * 1024u + lo4;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t hi = pack_bf16x2(x[j][0], x[j][1]);
-          const uint32_t lo = pack_bf16x2(x[j][0] - bf16lo_to_f32(hi), x[j][1] - bf16hi_to_f32(hi));
-          const uint32_t off = (uint32_t)(j >> 3) * 1024u + (uint32_t)(j & 7) * 128u + ((ch ^ (uint32_t)(j & 7)) << 4);
-          *reinterpret_cast<uint32_t*>(rb + off) = hi;
-          *reinterpret_cast<uint32_t*>(rb + pstride + off) = lo;
-        }
-        if (isg) {   // RPo % 16 == 0: the chunk lies in one output shell
-          const int o = row0 / p.RPo, rr = row0 - o * p.RPo;
-          float acc = 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc += sbeta[rr + j] * (x[j][0] + x[j][1]);
-#pragma unroll
-          for (int qo = 0; qo < 4; ++qo)
-            if (qo == o) dbacc[qo] += acc;
-        }
+  if (warp == kGWarpLD) {
+    // =========================== TMA loader ===========================
+    if (elect_one()) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[0]) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[1]) : "memory");
+    }
+    __syncwarp();
+    uint32_t s = 0, round = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      if (round > 0) mbar_wait_warp(&bars.empty[s], (round - 1) & 1);
+      if (elect_one()) {
+        uint8_t* st = smem + p.sm_ring + s * p.stage_bytes;
+        mbar_arrive_tx(&bars.full[s], 2 * (uint32_t)(p.GC + p.GR) * 128u);
+        tma_load_4d(st, &p.tm[1], 0, 0, 0, (int)t, &bars.full[s]);   // t = b * tiles_per_b + tile
+        tma_load_4d(st + p.cpart, &p.tm[1], 0, 0, 1, (int)t, &bars.full[s]);
+        tma_load_4d(st + 2 * p.cpart, &p.tm[0], 0, 0, 0, (int)t, &bars.full[s]);
+        tma_load_4d(st + 2 * p.cpart + p.gpart, &p.tm[0], 0, 0, 1, (int)t, &bars.full[s]);
       }
-      fence_proxy_async();   // generic-proxy tile writes -> visible to the tensor core
-      warp_arrive(&bars.tiles_full[buf]);
-    }
-    // ---- this CTA's Gram partial (after the last Gram MMA) ----
-    if (it > 0) mbar_wait_warp(&bars.gram_done[(it - 1) & 1], ((it - 1) >> 1) & 1);
-    fence_after();
-    const int qd = warp & 3, cg = warp >> 2, row = 32 * qd + lane;
-    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
-    float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
-    for (int ck = cg; ck < p.GC / 16; ck += 2) {   // block A: lane = g row, column = c row
-      float vv[16];
-      ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
-      if (row < p.GR)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = it > 0 ? vv[i] : 0.f;
-    }
-    if (p.GR > 128 && cg == 0) {
-      float vv[16];
-      ld16f(tq + p.colGB, vv);   // block B: lane = c row i (< 128), column = g row 128 + c
-      if (row < p.GC)
-#pragma unroll
-        for (int c = 0; c < 16; ++c)
-          if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = it > 0 ? vv[c] : 0.f;
-      if (p.GC > 128 && qd == 0) {
-        ld16f(tq + p.colGC, vv);   // block C (M = 64): lanes 0..15 = c rows 128..143
-        if (lane < 16 && 128 + lane < p.GC)
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = it > 0 ? vv[c] : 0.f;
+      __syncwarp();
+      if (++s == NS) {
+        s = 0;
+        ++round;
       }
-    }
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {   // fixed-order sums (no atomics): bitwise reproducible
-      float v = dbacc[o];
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) bars.db[warp][o] = v;
-    }
-    named_sync(1, kGMID * 32);
-    if (warp == 0 && lane < p.S_out) {
-      float v = 0.f;
-      for (int w = 0; w < kGMID; ++w) v += bars.db[w][lane];
-      p.partials[(int64_t)gridDim.x * p.GR * p.GC + (int64_t)blockIdx.x * p.S_out + lane] = v;
     }
   } else if (warp == kGWarpMMA) {
-    // =========================== MMA: G += g^T c per 16-voxel K-step, three blocks ===========================
+    // =========================== MMA: G += g^T c, three split products, three blocks ===========================
     const uint32_t idA = idesc_bf16(128, p.GC, 0, 0), idB = idesc_bf16(128, 16, 0, 0), idC = idesc_bf16(64, 16, 0, 0);
-    const uint32_t base = smem_u32(smem + p.sm_buf0);
-    uint32_t it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const uint32_t buf = it & 1;
-      mbar_wait_warp(&bars.tiles_full[buf], (it >> 1) & 1);
+    const uint32_t ring = smem_u32(smem + p.sm_ring);
+    uint32_t s = 0, round = 0;
+    bool first = true;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait_warp(&bars.full[s], round & 1);
       fence_after();
-      const uint32_t c0 = base + buf * p.buf_bytes, g0 = c0 + 2 * p.cpart;
+      const uint32_t c0 = ring + s * p.stage_bytes, g0 = c0 + 2 * p.cpart;
       for (int kk = 0; kk < kGV / 16; ++kk) {
         if (elect_one()) {
 #pragma unroll
@@ -1155,7 +1089,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
             const int i = Pairs<2>::i(k), j = Pairs<2>::j(k);
             const uint32_t gI = g0 + (uint32_t)i * p.gpart + kk * 32u, gJ = g0 + (uint32_t)j * p.gpart + kk * 32u;
             const uint32_t cI = c0 + (uint32_t)i * p.cpart + kk * 32u, cJ = c0 + (uint32_t)j * p.cpart + kk * 32u;
-            const uint32_t acc = (it > 0 || kk > 0 || k > 0) ? 1u : 0u;
+            const uint32_t acc = (!first || kk > 0 || k > 0) ? 1u : 0u;
             mma_ss(tbase + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
             if (p.GR > 128) {
               mma_ss(tbase + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
@@ -1167,35 +1101,44 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
         }
         __syncwarp();
       }
-      if (elect_one()) commit(&bars.gram_done[buf]);
+      if (elect_one()) commit(&bars.empty[s]);
       __syncwarp();
+      first = false;
+      if (++s == NS) {
+        s = 0;
+        ++round;
+      }
     }
-  } else if (p.tma) {
-    // =========================== TMA loader ===========================
-    if (elect_one()) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[0]) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&p.tm[1]) : "memory");
-    }
+    if (elect_one()) commit(&bars.done);
     __syncwarp();
-    const int sh = (int)(p.nvox & 3);
-    uint32_t s = 0, round = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t b = t / p.tiles_per_b;
-      const int v0 = (int)((t - b * p.tiles_per_b) * kGV);
-      for (int r = 0; r < per_tile; ++r) {
-        const int tensor = r < nG ? 0 : 1, j0 = 8 * (r < nG ? r : r - nG);
-        if (round > 0) role_wait(&bars.empty[s], (round - 1) & 1);
-        if (elect_one()) {
-          uint8_t* dst = smem + p.sm_ring + s * kGStage;
-          mbar_arrive_tx(&bars.full[s], kGStage);
-          tma_load_3d(dst, &p.tm[tensor], v0, j0, (int)b, &bars.full[s]);
-          tma_load_3d(dst + kGStage / 2, &p.tm[tensor], (int)p.nvox + v0 - sh, j0, (int)b, &bars.full[s]);
-        }
-        __syncwarp();
-        if (++s == NS) {
-          s = 0;
-          ++round;
-        }
+  } else {
+    // =========================== epilogue: this CTA's Gram partial ===========================
+    mbar_wait_warp(&bars.done, 0);
+    fence_after();
+    const bool any = ntiles > (int64_t)blockIdx.x;
+    const int qd = warp & 3, row = 32 * qd + lane;
+    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
+    float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
+    for (int ck = 0; ck < p.GC / 16; ++ck) {   // block A: lane = g row, column = c row
+      float vv[16];
+      ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
+      if (row < p.GR)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = any ? vv[i] : 0.f;
+    }
+    if (p.GR > 128) {
+      float vv[16];
+      ld16f(tq + p.colGB, vv);   // block B: lane = c row i (< 128), column = g row 128 + c
+      if (row < p.GC)
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = any ? vv[c] : 0.f;
+      if (p.GC > 128 && qd == 0) {
+        ld16f(tq + p.colGC, vv);   // block C (M = 64): lanes 0..15 = c rows 128..143
+        if (lane < 16 && 128 + lane < p.GC)
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = any ? vv[c] : 0.f;
       }
     }
   }
@@ -1238,8 +1181,8 @@ __global__ void gram_reduce_k(const float* __restrict__ partials, double* __rest
   }
 }
 
-// dW[o,s,k] = <P_k, G_{o,s}> and db[o] = sum of the per-CTA beta . g partials, in float64
-__global__ void gram_finalize_k(const double* __restrict__ G, const float* __restrict__ dbparts, int nparts,
+// dW[o,s,k] = <P_k, G_{o,s}> and db[o] = beta . G[o-block rows][ones column] (= beta . sum_v g_v), in float64
+__global__ void gram_finalize_k(const double* __restrict__ G, const float* __restrict__ beta, int ones,
                                 const float* __restrict__ P, float* __restrict__ dW, float* __restrict__ db, int s_out,
                                 int s_in, int K, int r_out, int r_in, int RPo, int RPi) {
   __shared__ double red[32];
@@ -1255,7 +1198,8 @@ __global__ void gram_finalize_k(const double* __restrict__ G, const float* __res
     }
   } else {
     const int o = id - nw;
-    for (int q = threadIdx.x; q < nparts; q += blockDim.x) acc += (double)__ldg(dbparts + (int64_t)q * s_out + o);
+    for (int r = threadIdx.x; r < r_out; r += blockDim.x)
+      acc += (double)__ldg(beta + r) * G[(int64_t)(o * RPo + r) * GC + ones];
   }
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -1454,21 +1398,19 @@ bool use_v3() {
 }
 
 bool plan_gram(GramP& p) {
-  if (p.GR > 144 || p.GC > 144 || p.S_out > 4 || p.GR % 16 || p.GC % 16) return false;
+  if (p.GR > 144 || p.GC > 144 || p.GR % 16 || p.GC % 16) return false;
   const int grow = p.GR < 128 ? 128 : p.GR;
   p.colGA = 0;
   p.colGB = (uint32_t)p.GC;
   p.colGC = (uint32_t)p.GC + 16;
-  p.cpart = (uint32_t)(p.GC / 8) * 1024u;
-  p.gpart = (uint32_t)(grow / 8) * 1024u;
-  p.buf_bytes = 2 * p.cpart + 2 * p.gpart;   // block C over-reads c rows up to 191: they land in what follows
-  size_t o = 0;
-  p.sm_buf0 = (uint32_t)o; o = al(o + 2 * (size_t)p.buf_bytes + 8192, 1024);
-  p.sm_beta = (uint32_t)o; o = al(o + (size_t)p.RPo * 4, 128);
-  p.sm_ring = (uint32_t)o;
-  for (int ns : {16, 8}) {
+  p.cpart = (uint32_t)p.GC * 128u;   // rows x one 128-byte K atom (64 bf16 voxels)
+  p.gpart = (uint32_t)grow * 128u;
+  // block C reads c rows up to 191 of a term plane: they land in the next plane of the same stage
+  p.stage_bytes = (uint32_t)al(2 * (size_t)p.cpart + 2 * (size_t)p.gpart, 1024);
+  p.sm_ring = 0;
+  for (int ns : {4, 3, 2}) {
     p.ns = ns;
-    size_t q = al(p.sm_ring + (size_t)p.ns * kGStage, 16);
+    size_t q = al((size_t)ns * p.stage_bytes, 16);
     p.sm_bar = (uint32_t)q;
     q = al(q + sizeof(BarsG), 16);
     p.smem_bytes = (uint32_t)q;
@@ -1521,8 +1463,9 @@ int launch_gram(const GramP& p, int grid, cudaStream_t st) {
 
 int run_gram(const GramP& p, int grid, cudaStream_t st) {
   switch (p.ns) {
-    case 8: return launch_gram<8>(p, grid, st);
-    default: return launch_gram<16>(p, grid, st);
+    case 2: return launch_gram<2>(p, grid, st);
+    case 3: return launch_gram<3>(p, grid, st);
+    default: return launch_gram<4>(p, grid, st);
   }
 }
 
@@ -1572,23 +1515,20 @@ Chain3 chain3_params(const Dims& d, const WsLayout& w, const uint8_t* ws, bool a
   return p;
 }
 
+int64_t mid_pitch(int64_t nvox) { return (nvox + kGV - 1) / kGV * kGV; }
+
 GramP gram_params(const Dims& d, const WsLayout& w, uint8_t* ws) {
   GramP p{};
   p.nbatch = d.nbatch;
-  p.nvox = d.nvox;
-  p.tiles_per_b = (d.nvox + kGV - 1) / kGV;
+  p.tiles_per_b = mid_pitch(d.nvox) / kGV;
   p.GR = d.s_out * d.RPo;
   p.GC = d.s_in * d.RPi;
-  p.S_out = d.s_out;
-  p.RPo = d.RPo;
-  p.R_out = d.r_out;
   p.partials = reinterpret_cast<float*>(ws + w.parts);
-  p.g_bs = (int64_t)p.GR * d.nvox;
-  p.c_bs = (int64_t)p.GC * d.nvox;
   return p;
 }
 
 bool chain_fits(const Dims& d) {
+  if (d.RPi == d.r_in) return false;   // the Gram's bias column needs a zero-weight padding row in c
   Chain3 f = chain3_params(d, ws_layout(d, 1), nullptr, false);
   Chain3 a = chain3_params(d, ws_layout(d, 1), nullptr, true);
   GramP g = gram_params(d, ws_layout(d, 1), nullptr);
@@ -1602,8 +1542,18 @@ bool chain_fits(const Dims& d) {
 // Channel-pair view of a (nbatch, rows, nvox) fp32 tensor for TMA: element (u, j, b) is channel 2j + u / nvox,
 // voxel u % nvox -- rows 2j and 2j+1 are contiguous, so the row stride 8*nvox bytes is 16-byte aligned for
 // any even nvox.  Box = 132 voxels x 8 channel pairs.  False (use the cp.async path) if not expressible.
-bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, int64_t group_rows, int64_t nvox,
-              int boxv = kBoxV) {
+CUtensorMapL2promotion l2_promotion() {   // tuning knob DELIMIT_L2_PROMO = 0 / 64 / 128 / 256 (default)
+  static const CUtensorMapL2promotion v = [] {
+    const char* e = getenv("DELIMIT_L2_PROMO");
+    const int b = e ? atoi(e) : 256;
+    return b == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : b == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : b == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return v;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1614,6 +1564,12 @@ bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, i
     }
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
+  return encode;
+}
+
+bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, int64_t group_rows, int64_t nvox,
+              int boxv = kBoxV) {
+  auto encode = tensor_map_encoder();
   if (!encode || !base || nvox % 2 || rows % 2 || group_rows % 2 || ((uintptr_t)base & 15) ||
       2 * nvox + kTileV >= ((int64_t)1 << 31) || nbatch >= ((int64_t)1 << 31) || rows / 2 > ((int64_t)1 << 31))
     return false;
@@ -1622,7 +1578,23 @@ bool pair_map(CUtensorMap* m, const float* base, int64_t nbatch, int64_t rows, i
   const cuuint32_t box[3] = {(cuuint32_t)boxv, 8u, 1u};
   const cuuint32_t es[3] = {1u, 1u, 1u};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tiled mid buffer [b][64-voxel tile][term][row][64 voxels] bf16 as a 4-D map (64, rows, 2, nbatch * tiles):
+// one box = one term plane of one tile, a contiguous rows x 128-byte block; SWIZZLE_128B makes TMA write
+// exactly the K-major operand layout desc_sw128_k reads.
+bool mid_map(CUtensorMap* m, const void* base, int64_t nbatch, int rows, int64_t pitch) {
+  auto encode = tensor_map_encoder();
+  const int64_t nt = nbatch * (pitch / kGV);
+  if (!encode || !base || ((uintptr_t)base & 15) || rows > 256 || nt >= ((int64_t)1 << 31)) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)kGV, (cuuint64_t)rows, 2, (cuuint64_t)nt};
+  const cuuint64_t strides[3] = {(cuuint64_t)(2 * kGV), (cuuint64_t)(2 * kGV * rows), (cuuint64_t)(4 * kGV * rows)};
+  const cuuint32_t box[4] = {(cuuint32_t)kGV, (cuuint32_t)rows, 1u, 1u};
+  const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1658,9 +1630,12 @@ size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int
   return ws_layout(make_dims(nbatch, s_in, s_out, n, r_in, r_out, n_out, nvox, 1), kMaxParts).total;
 }
 
-int64_t dl_chain_mid_rows(int64_t shells, int64_t r) { return shells * ((r + 15) / 16 * 16); }
+size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvox) {
+  using namespace dl::tc;
+  return (size_t)nbatch * 2 * (size_t)(shells * r16(r)) * (size_t)mid_pitch(nvox) * 2;
+}
 
-int dl_chain_fwd_f32(const float* x, float* y, float* c_mid, const float* M, int m_per_shell, const float* L,
+int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
                      const float* bvec, const float* Bt, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out,
                      int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   using namespace dl::tc;
@@ -1680,8 +1655,10 @@ int dl_chain_fwd_f32(const float* x, float* y, float* c_mid, const float* M, int
   DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
   p.in = x;
   p.out = y;
-  p.mid = c_mid;
-  p.mid_bs = (int64_t)d.s_in * d.RPi * nvox;
+  p.mid = reinterpret_cast<uint16_t*>(c_mid);
+  p.mid_pitch = mid_pitch(nvox);
+  p.mid_bs = 2 * (int64_t)d.s_in * d.RPi * p.mid_pitch;
+  p.mid_ones = d.r_in;   // shell 0's first padding row
   p.bias2 = bvec;
   p.prof = g_prof;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
@@ -1689,7 +1666,7 @@ int dl_chain_fwd_f32(const float* x, float* y, float* c_mid, const float* M, int
   return run_chain(p, d, grid, st, "chain_fwd");
 }
 
-int dl_chain_bwd_f32(const float* c_mid, const float* dy, float* dx, float* dW, float* db, float* g_mid,
+int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
                      const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
                      const float* beta, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K,
                      int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
@@ -1712,8 +1689,10 @@ int dl_chain_bwd_f32(const float* c_mid, const float* dy, float* dx, float* dW, 
     Chain3 p = chain3_params(d, w, ws, true);
     p.in = dy;
     p.out = dx;
-    p.mid = wgrad ? g_mid : nullptr;
-    p.mid_bs = (int64_t)d.s_out * d.RPo * nvox;
+    p.mid = wgrad ? reinterpret_cast<uint16_t*>(g_mid) : nullptr;
+    p.mid_pitch = mid_pitch(nvox);
+    p.mid_bs = 2 * (int64_t)d.s_out * d.RPo * p.mid_pitch;
+    p.mid_ones = -1;
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
     DL_TRY(run_chain(p, d, grid_for(ntiles, sm), st, "chain_bwd"));
@@ -1725,24 +1704,20 @@ int dl_chain_bwd_f32(const float* c_mid, const float* dy, float* dx, float* dW, 
     const int64_t gtiles = nbatch * g.tiles_per_b;
     int nparts = 0;
     if (gtiles > 0) {
-      g.g = g_mid;
-      g.c = c_mid;
-      g.beta = beta;
-      g.tma = !tma_disabled() && pair_map(&g.tm[0], g_mid, nbatch, GR, d.RPo, nvox, kGBoxV) &&
-              pair_map(&g.tm[1], c_mid, nbatch, GC, d.RPi, nvox, kGBoxV);
+      DL_REQUIRE(mid_map(&g.tm[0], g_mid, nbatch, GR, mid_pitch(nvox)) &&
+                     mid_map(&g.tm[1], c_mid, nbatch, GC, mid_pitch(nvox)),
+                 "chain_bwd: c_mid / g_mid must be 16-byte aligned buffers of dl_chain_mid_bytes()");
       nparts = grid_for(gtiles, sm < kMaxParts ? sm : kMaxParts);
       DL_TRY(run_gram(g, nparts, st));
     }
-    float* partials = reinterpret_cast<float*>(ws + w.parts);
     double* G = reinterpret_cast<double*>(ws + w.G);
     if (nparts == 0) {
       DL_CUDA(cudaMemsetAsync(G, 0, (size_t)GR * GC * 8, st));
     } else {
-      gram_reduce_k<<<(GR * GC + 255) / 256, 256, 0, st>>>(partials, G, nparts, GR * GC);
+      gram_reduce_k<<<(GR * GC + 255) / 256, 256, 0, st>>>(reinterpret_cast<float*>(ws + w.parts), G, nparts, GR * GC);
       DL_TRY(dl::after_launch("gram_reduce"));
     }
-    const float* dbparts = partials + (size_t)nparts * GR * GC;
-    gram_finalize_k<<<(unsigned)(s_out * s_in * K + s_out), 256, 0, st>>>(G, dbparts, nparts, P, dW, db, (int)s_out,
+    gram_finalize_k<<<(unsigned)(s_out * s_in * K + s_out), 256, 0, st>>>(G, beta, (int)r_in, P, dW, db, (int)s_out,
                                                                           (int)s_in, (int)K, (int)r_out, (int)r_in,
                                                                           d.RPo, d.RPi);
     DL_TRY(dl::after_launch("gram_finalize"));

@@ -150,10 +150,11 @@ class LscFunction(torch.autograd.Function):
 class ChainFunction(torch.autograd.Function):
     """Fused Signal2SH -> LSC -> SH2Signal on tcgen05 (dl_chain_fwd_f32 / dl_chain_bwd_f32).
 
-    Forward is one kernel (x -> y) that also writes the Signal2SH coefficients c = M x
-    (zero-padded rows, `c_mid`) for the weight gradient; x itself is not kept.  Backward is
-    one kernel for dx (the adjoint chain, which writes g = B'^T dy to `g_mid`), one Gram
-    kernel over (g_mid, c_mid) for the LSC parameters, and a float64 finalize.
+    Forward is one kernel (x -> y) that also writes the Signal2SH coefficients c = M x as
+    two-term bf16 planes (`c_mid`, the Gram operand) for the weight gradient; x itself is not
+    kept.  Backward is one kernel for dx (the adjoint chain, which writes g = B'^T dy the same
+    way to `g_mid`), one streaming Gram kernel over (g_mid, c_mid) for the LSC parameters, and
+    a float64 finalize.
     """
 
     @staticmethod
@@ -167,8 +168,7 @@ class ChainFunction(torch.autograd.Function):
         want_w = ctx.needs_input_grad[1] or (bias is not None and ctx.needs_input_grad[2])
         L, _, bvec = build_lsc_operator(fold, beta, weight, bias, want_Lt=False)
         y = torch.empty((B, s_out * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
-        c_mid = (torch.empty((B, lib.dl_chain_mid_rows(s_in, r_in), V), dtype=torch.float32, device=x.device)
-                 if want_w else None)
+        c_mid = _workspace(lib.dl_chain_mid_bytes(B, s_in, r_in, V), x.device) if want_w else None
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
         _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(c_mid), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt),
                   _p(ws), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
@@ -197,8 +197,7 @@ class ChainFunction(torch.autograd.Function):
         dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
         dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=dy.device) if want_w else None
         db = torch.empty((s_out,), dtype=torch.float32, device=dy.device) if want_b else None
-        g_mid = (torch.empty((B, lib.dl_chain_mid_rows(s_out, r_out), V), dtype=torch.float32, device=dy.device)
-                 if (want_w or want_b) else None)
+        g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device) if (want_w or want_b) else None
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
         _lib.call("dl_chain_bwd_f32", _p(c_mid), _p(dy), _p(dx), _p(dW), _p(db), _p(g_mid), _p(M),
                   int(ctx.per_shell), _p(L), _p(Bt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out,
