@@ -75,7 +75,7 @@ class ClockSampler:
         self.uuid = uuid
 
     def start(self):
-        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"]
+        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20"]
         if self.uuid:
             cmd += ["-i", self.uuid]
         try:
@@ -237,6 +237,42 @@ def run_ours(args):
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
+    if not args.no_graph:
+        # Replay the step as two CUDA graphs (forward, backward): the same kernels and buffers, without
+        # ~20 host launches and the Python/autograd work between them.  Gradients are written (not
+        # accumulated) on every replay, exactly like the eager step with .grad reset to None.
+        x.grad = None
+        for p in params:
+            p.grad = None
+        pool = torch.cuda.graph_pool_handle()
+        g_fwd, g_bwd = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        c0 = _lib.total_launches()
+        with torch.cuda.graph(g_fwd, pool=pool):
+            y_static = chain(x)
+        with torch.cuda.graph(g_bwd, pool=pool):
+            y_static.backward(dy)
+        torch.cuda.synchronize()
+        graph_launches = _lib.total_launches() - c0   # our kernels captured per step
+
+        def step(record):  # noqa: F811 -- graphed replacement of the eager step above
+            if record:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record()
+            g_fwd.replay()
+            if record:
+                e1.record()
+            g_bwd.replay()
+            if record:
+                e2.record()
+                fwd_ev.append((e0, e1))
+                bwd_ev.append((e1, e2))
+            if world > 1:
+                allreduce_gradients(params)
+            return y_static
+
+        for _ in range(args.warmup):
+            step(False)
+        torch.cuda.synchronize()
     uuid = None
     try:
         uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
@@ -258,6 +294,8 @@ def run_ours(args):
     end.record()
     torch.cuda.synchronize()
     launches = _lib.total_launches() - n0
+    if not args.no_graph:
+        launches = graph_launches * args.steps   # replays do not pass through the host launch counter
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
@@ -330,7 +368,8 @@ def run_ours(args):
                                    "pi/5) -> SH2Signal fwd+bwd, one 145x174x145 subject per GPU",
                        "model": "SphericalChain", "global_batch": world, "voxels_per_gpu": V,
                        "channels": SHELLS * NDIR, "seq_len": None, "parallelism": f"dp{world} (subject-sharded)",
-                       "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2"},
+                       "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2",
+                       "cuda_graph": not args.no_graph},
             "roofline": {"bound": "hbm", "kernel": "chain3v_tc (forward)", "achieved": achieved, "peak": peak,
                          "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
@@ -359,6 +398,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time the eager autograd step instead of its CUDA graphs")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
