@@ -681,6 +681,7 @@ struct Bars3v {
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];
   uint64_t d1_full, d2_full, d3_full, d3_free;
+  uint64_t d1_read;   // OUT has stored D1(t) to the mid buffer: the MMA may overwrite D1
   uint32_t tmem_base;
 };
 
@@ -726,6 +727,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     mbar_init(&bars.d2_full, 1);
     mbar_init(&bars.d3_full, 1);
     mbar_init(&bars.d3_free, kOUT3);
+    mbar_init(&bars.d1_read, kOUT3);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -792,9 +794,6 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         }
         uint32_t w[PARTS][8];
         split16<PARTS>(v, w);
-        if (i < nk2 && p.mid && vx < p.mid_pitch)
-          store_mid(p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2 + 16 * i) * 64 + (vx & 63), (int64_t)K2 * 64,
-                    64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
         if (cround > 0) role_wait(&bars.c_empty[cslot], (cround - 1) & 1);
         fence_after();
         store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
@@ -819,6 +818,22 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
+      // the stage-1 accumulator's first two split terms -> the tiled mid buffer (c for the Gram in the
+      // forward, g in the adjoint); OUT is otherwise idle while the conversions of stage 2 run
+      role_wait(&bars.d1_full, it & 1);
+      fence_after();
+      if (p.mid && v < p.mid_pitch) {
+        for (int ck = cg; ck < K2 / 16; ck += kOUTQ) {
+          float vv[16];
+          ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
+          uint32_t w[2][8];
+          split16<2>(vv, w);
+          store_mid(p.mid + ((b * (p.mid_pitch >> 6) + (v >> 6)) * 2 * K2 + 16 * ck) * 64 + (v & 63), (int64_t)K2 * 64,
+                    64, w[0], w[1], vok ? p.mid_ones - 16 * ck : -1);
+        }
+      }
+      fence_before();
+      warp_arrive(&bars.d1_read);
       for (int o = 0; o < p.G2; ++o, ++n3) {
         role_wait(&bars.d3_full, n3 & 1);
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
@@ -979,8 +994,13 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #pragma unroll
         for (int j = 0; j < PARTS; ++j) bg3[j] += g3s;
         DL_PROF(2, 3 + 2 * o);
-        if (next)
+        if (next) {
+          if (o == 0) {   // D1(t) must also have been stored to the mid buffer before stage 1 overwrites it
+            mbar_wait_warp(&bars.d1_read, it & 1);
+            fence_after();
+          }
           for (const int qe = n1 * (o + 1) / p.G2; q1 < qe; ++q1) s1_next();
+        }
       }
     }
   } else if (p.tma) {
