@@ -162,6 +162,20 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
+// Waits of roles off the critical path (IN ahead of the MMA, OUT between drains) can back off so their
+// polling does not take issue slots from the MMA warp on the same scheduler (DL_IDLE_NS, 0 = spin).
+#ifndef DL_IDLE_NS
+#define DL_IDLE_NS 0
+#endif
+#ifndef DL_IDLE_MASK
+#define DL_IDLE_MASK 3   // bit 0: IN waits, bit 1: OUT waits
+#endif
+template <int ROLE>
+__device__ __forceinline__ void idle_wait(uint64_t* bar, uint32_t parity) {
+  if (DL_IDLE_NS > 0 && (DL_IDLE_MASK & (1 << ROLE))) mbar_wait_sleep(bar, parity, DL_IDLE_NS);
+  else mbar_wait_warp(bar, parity);
+}
+
 // wait used by the IN / CONV / OUT / loader roles (the MMA warp keeps mbar_wait_warp)
 __device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) {
   if (kSleepNs) mbar_wait_sleep(bar, parity, kSleepNs);
@@ -200,7 +214,7 @@ __device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int
                                       uint64_t* a_empty, uint32_t& aslot, uint32_t& around, int step = 1) {
   uint32_t w[PARTS][8];
   split16<PARTS>(v, w);
-  if (around > 0) role_wait(&a_empty[aslot], (around - 1) & 1);
+  if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
   fence_after();
   store_parts<PARTS>(tslots + aslot * (PARTS * 8), 8, w);
   tmem_wait_st();
@@ -322,7 +336,7 @@ __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_
       if ((q & (uint32_t)(nIW - 1)) != (uint32_t)iw) continue;
       const ChunkGeo cg = geo(r);
       const int nval = vok ? cg.nval : 0;   // voxels past nvox read neighbouring-row data: zero them
-      role_wait(&full[cs], cround & 1);
+      idle_wait<0>(&full[cs], cround & 1);
       const float* rp = ring + cs * (kStageBytes / 4) + 32 * qd + lane;
       float v[16];
 #pragma unroll
@@ -820,7 +834,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       const bool vok = v < p.nvox;
       // the stage-1 accumulator's first two split terms -> the tiled mid buffer (c for the Gram in the
       // forward, g in the adjoint); OUT is otherwise idle while the conversions of stage 2 run
-      role_wait(&bars.d1_full, it & 1);
+      idle_wait<1>(&bars.d1_full, it & 1);
       fence_after();
       if (p.mid && v < p.mid_pitch) {
         for (int ck = cg; ck < K2 / 16; ck += kOUTQ) {
@@ -835,7 +849,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       fence_before();
       warp_arrive(&bars.d1_read);
       for (int o = 0; o < p.G2; ++o, ++n3) {
-        role_wait(&bars.d3_full, n3 & 1);
+        idle_wait<1>(&bars.d3_full, n3 & 1);
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
         fence_after();
         for (int ck = cg; ck < p.N3 / 16; ck += kOUTQ) {

@@ -20,7 +20,38 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
   __syncthreads();
   fence_after();
   const uint32_t tb = tb_s;
-  if (mode >= 40) {
+  if (mode >= 50) {
+    // kernel-like B operand: K-major core-matrix image of N rows x Kc cols (SBO = Kc/8*128, LBO = 128),
+    // 6 split-pair TS MMAs per K-step, K-step advance = 256 bytes; mode 51: MN-major (LBO = Nc/8*128, SBO = 128)
+    const uint32_t sbb = smem_u32(smem);
+    const uint32_t id = idesc_bf16(128, N, 0, mode == 51 ? 1 : 0);
+    const int Kc = 144;
+    if (warp == 0) {
+      uint64_t bd[3];
+      for (int j = 0; j < 3; ++j)
+        bd[j] = mode == 51 ? desc_noswz(sbb + j * 9216, (uint32_t)(N / 8) * 128u, 128)
+                           : desc_noswz(sbb + j * 9216, 128, (uint32_t)(Kc / 8) * 128u);
+      const uint64_t ks = mode == 51 ? (uint64_t)((2u * (uint32_t)(N / 8) * 128u) >> 4) : (uint64_t)(256 >> 4);
+      long long t0 = clock64();
+      for (int k = 0; k < iters / 6; ++k) {
+        if (elect_one()) {
+          mma_ts(tb + dcol, tb + acol + 16, bd[0], id, k > 0);
+          mma_ts(tb + dcol, tb + acol + 8, bd[1], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[2], id, 1);
+          mma_ts(tb + dcol, tb + acol + 8, bd[0], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[1], id, 1);
+          mma_ts(tb + dcol, tb + acol, bd[0], id, 1);
+        }
+        __syncwarp();
+        for (int j = 0; j < 3; ++j) bd[j] += ((k & 7) == 7) ? (uint64_t)0 - 7 * ks : ks;
+      }
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+      mbar_wait(&mbar, 0);
+      long long t1 = clock64();
+      if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; }
+    }
+  } else if (mode >= 40) {
     // kernel-pattern probe: 6 TS MMAs (3x3 split pairs) per step, plus optional commit / fence / poll
     __shared__ uint64_t mb2, mb3;
     if (threadIdx.x == 0) { mbar_init(&mb2, 1); mbar_init(&mb3, 1); mbar_fence_init(); mbar_arrive(&mb3); }
@@ -56,7 +87,7 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
     }
   } else if (mode >= 30) {
     // warp 0 issues TS MMAs (D at dcol, A at acol); warps 4..7 generate TMEM traffic meanwhile:
-    // mode 30 none, 31 tcgen05.ld x16, 32 tcgen05.st x16, 33 both
+    // mode 30 none, 31 tcgen05.ld x16, 32 tcgen05.st x16, 33 both, +4 shared-memory traffic (warps 4..15)
     __shared__ volatile int stop;
     if (threadIdx.x == 0) stop = 0;
     __syncthreads();
@@ -79,11 +110,20 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
       uint32_t r[16];
       for (int i = 0; i < 16; ++i) r[i] = i;
       long long n = 0;
+      volatile float* sm = reinterpret_cast<volatile float*>(smem);   // first 32 KB: the A image, unused by TS
+      float acc = 0.f;
       while (!stop) {
         if (mode & 1) { tmem_ld<16>(ta, r); tmem_wait_ld(); }
         if (mode & 2) { tmem_st<16>(ta + 16, r); tmem_wait_st(); }
+        if (mode & 4) {   // shared-memory traffic: 16 x 128-byte warp loads + stores
+          for (int k = 0; k < 16; ++k) {
+            acc += sm[(k * 1024 + (threadIdx.x & 31) * 4 + (warp & 3) * 128) & 8191];
+            sm[((k * 1024 + (threadIdx.x & 31) * 4 + 4096) & 8191)] = acc;
+          }
+        }
         ++n;
       }
+      if (acc == 1.2345f) out[1] = 0;
       if ((threadIdx.x & 31) == 0 && warp == 4) out[1] = n;
     }
   } else if (mode >= 20) {
@@ -156,7 +196,7 @@ extern "C" int mma_rate(int mode, int N, int iters, long long* out_host, int dco
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  rate_k<<<1, 256, 64 * 1024>>>(mode, N, iters, d, dcol, acol);
+  rate_k<<<1, mode >= 30 && mode < 40 ? 512 : 256, 64 * 1024>>>(mode, N, iters, d, dcol, acol);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(out_host, d, 16, cudaMemcpyDeviceToHost);
   cudaFree(d);
