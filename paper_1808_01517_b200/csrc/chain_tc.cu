@@ -686,8 +686,9 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
 #endif
 constexpr int kCVQ = DL_CV_PER_Q, kOUTQ = DL_OUT_PER_Q;   // CONV / OUT warps per TMEM lane quadrant
 constexpr int kIN3 = 8, kCV3 = 4 * kCVQ, kOUT3 = 4 * kOUTQ;
-constexpr int kW3MMA = kIN3 + kCV3 + kOUT3;   // 24
-constexpr int kW3LD = kW3MMA + 1;             // 25
+constexpr int kW3MMA = kIN3 + kCV3 + kOUT3;   // 24: stage-1 MMA issuer (+ TMEM owner)
+constexpr int kW3MMA2 = kW3MMA + 1;           // 25: stage-2/3 MMA issuer
+constexpr int kW3LD = kW3MMA2 + 1;            // 26
 constexpr int kThreads3 = (kW3LD + 1) * 32;
 
 struct Bars3v {
@@ -696,6 +697,7 @@ struct Bars3v {
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];
   uint64_t d1_full, d2_full, d3_full, d3_free;
   uint64_t d1_read;   // OUT has stored D1(t) to the mid buffer: the MMA may overwrite D1
+  uint64_t s2_taken;  // the stage-2/3 issuer holds every D1(t) conversion: D1 may be overwritten
   uint32_t tmem_base;
 };
 
@@ -742,6 +744,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     mbar_init(&bars.d3_full, 1);
     mbar_init(&bars.d3_free, kOUT3);
     mbar_init(&bars.d1_read, kOUT3);
+    mbar_init(&bars.s2_taken, 1);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -878,8 +881,11 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         if (ow == 0) DL_PROF(1, 9 + 2 * o);
       }
     }
-  } else if (warp == kW3MMA) {
-    // =========================== MMA issuer ===========================
+  } else if (warp == kW3MMA || warp == kW3MMA2) {
+    // =========================== MMA issuers ===========================
+    // Two issuing warps on different schedulers: under contention each tcgen05.mma costs the issuing
+    // warp ~100 cycles of issue latency, so stage 1 (fed by IN) and stages 2/3 (fed by CONV) get one
+    // warp each and the tensor pipe interleaves them.
     // Lean loop: descriptors advance by additions; stage/group cursors are incremental.
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2), sw3 = smem_u32(smem + p.sm_w3);
     const int km = p.adjoint ? 0 : 1;
@@ -903,117 +909,110 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
     const uint32_t tA = tbase + p.colA, tC = tbase + p.colC, tD1 = tbase + p.colD1, tD2 = tbase + p.colD2,
                    tD3 = tbase + p.colD3;
-    // Static issue order per tile t: stage 2(t); then for each output group o: stage 3(t, o) followed by
-    // a share of stage 1(t+1) -- those MMAs run while OUT drains D3(o).  All waits block (no polling).
-    // The MMA warp is instruction-latency bound (it shares its scheduler with six other warps), so
-    // every cursor below advances by additions only.
     uint32_t aslot = 0, around = 0, cslot = 0, cround = 0, n3 = 0;
     uint32_t aaddr = tA, caddr = tC;
-    int g1 = 0, k1 = 0;
-    uint32_t d1col = tD1;
-    uint64_t bd1[PARTS];
-#pragma unroll
-    for (int j = 0; j < PARTS; ++j) bd1[j] = B1[j];
-    auto s1_next = [&]() {   // next stage-1 K-step (input chunk) in (group, k) order
-      mbar_wait_warp(&bars.a_full[aslot], around & 1);
-      fence_after();
-      const bool first = k1 == 0, last = k1 == nk1 - 1 && g1 == p.G1 - 1;
-      if (elect_one()) {
-        kstep_ts<PARTS>(d1col, aaddr, 8, bd1, id1, first);
-        commit(&bars.a_empty[aslot]);
-        if (last) commit(&bars.d1_full);
-      }
-      __syncwarp();
-      if (++aslot == (uint32_t)p.NA) {
-        aslot = 0;
-        ++around;
-        aaddr = tA;
-      } else {
-        aaddr += kSlotW;
-      }
-      if (++k1 == nk1) {
-        k1 = 0;
-        if (++g1 == p.G1) g1 = 0;
-        d1col = tD1 + (uint32_t)(g1 * p.N1);
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd1[j] = B1[j] + (uint64_t)g1 * g1s;
-      } else {
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd1[j] += ks1;
-      }
-    };
-    auto c_take = [&]() {   // wait for the next conversion-ring item
-      mbar_wait_warp(&bars.c_full[cslot], cround & 1);
-      fence_after();
-    };
-    auto c_release = [&](uint64_t* extra) {
-      if (elect_one()) {
-        commit(&bars.c_empty[cslot]);
-        if (extra) commit(extra);
-      }
-      __syncwarp();
-      if (++cslot == (uint32_t)p.NAc) {
-        cslot = 0;
-        ++cround;
-        caddr = tC;
-      } else {
-        caddr += kSlotW;
-      }
-    };
     const int n1 = p.G1 * nk1;
-    for (int q = 0; q < (nmine > 0 ? n1 : 0); ++q) s1_next();
-    for (uint32_t it = 0; it < nmine; ++it) {
-      DL_PROF(2, 0);
-      // ---- stage 2 ----
-      uint64_t bd2[PARTS];
-#pragma unroll
-      for (int j = 0; j < PARTS; ++j) bd2[j] = B2[j];
-      for (int jj = 0; jj < nk2; ++jj) {
-        c_take();
-        uint64_t bd[PARTS];
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd[j] = bd2[j];
-        for (int oo = 0; oo < n2m; ++oo) {
-          if (elect_one()) kstep_ts<PARTS>(tD2 + (uint32_t)(oo * p.N2), caddr, 8, bd, id2, jj == 0);
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) bd[j] += o2s;
+    if (warp == kW3MMA) {
+      // ---- stage 1: input chunks -> D1, tile after tile ----
+      for (uint32_t it = 0; it < nmine; ++it) {
+        if (it > 0) {   // D1(t-1) fully converted (issuer 2 took every stage-2 item) and stored (OUT)
+          mbar_wait_warp(&bars.s2_taken, (it - 1) & 1);
+          mbar_wait_warp(&bars.d1_read, (it - 1) & 1);
+          fence_after();
         }
-        c_release(jj == nk2 - 1 ? &bars.d2_full : nullptr);
+        uint32_t d1col = tD1;
+        for (int g = 0; g < p.G1; ++g, d1col += (uint32_t)p.N1) {
+          uint64_t bd[PARTS];
 #pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd2[j] += ks2;
-      }
-      DL_PROF(2, 1);
-      // ---- stage 3 per output group, interleaved with the next tile's stage 1 ----
-      const bool next = it + 1 < nmine;
-      int q1 = 0;
-      uint64_t bg3[PARTS];
-#pragma unroll
-      for (int j = 0; j < PARTS; ++j) bg3[j] = B3[j];
-      for (int o = 0; o < p.G2; ++o) {
-        if (n3 > 0) mbar_wait_warp(&bars.d3_free, (n3 - 1) & 1);
-        DL_PROF(2, 2 + 2 * o);
-        uint64_t bd[PARTS];
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bd[j] = bg3[j];
-        for (int jj = 0; jj < nk3; ++jj) {
-          c_take();
-          if (elect_one()) kstep_ts<PARTS>(tD3, caddr, 8, bd, id3, jj == 0);
-          __syncwarp();
-          c_release(jj == nk3 - 1 ? &bars.d3_full : nullptr);
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) bd[j] += ks3;
-        }
-        ++n3;
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bg3[j] += g3s;
-        DL_PROF(2, 3 + 2 * o);
-        if (next) {
-          if (o == 0) {   // D1(t) must also have been stored to the mid buffer before stage 1 overwrites it
-            mbar_wait_warp(&bars.d1_read, it & 1);
+          for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s;
+          for (int k = 0; k < nk1; ++k) {
+            mbar_wait_warp(&bars.a_full[aslot], around & 1);
             fence_after();
+            const bool last = k == nk1 - 1 && g == p.G1 - 1;
+            if (elect_one()) {
+              kstep_ts<PARTS>(d1col, aaddr, 8, bd, id1, k == 0);
+              commit(&bars.a_empty[aslot]);
+              if (last) commit(&bars.d1_full);
+            }
+            __syncwarp();
+            if (++aslot == (uint32_t)p.NA) {
+              aslot = 0;
+              ++around;
+              aaddr = tA;
+            } else {
+              aaddr += kSlotW;
+            }
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] += ks1;
           }
-          for (const int qe = n1 * (o + 1) / p.G2; q1 < qe; ++q1) s1_next();
+        }
+      }
+    } else {
+      // ---- stages 2 and 3: conversion-ring items in CONV order ----
+      auto c_take = [&]() {
+        mbar_wait_warp(&bars.c_full[cslot], cround & 1);
+        fence_after();
+      };
+      auto c_release = [&](uint64_t* extra) {
+        if (elect_one()) {
+          commit(&bars.c_empty[cslot]);
+          if (extra) commit(extra);
+        }
+        __syncwarp();
+        if (++cslot == (uint32_t)p.NAc) {
+          cslot = 0;
+          ++cround;
+          caddr = tC;
+        } else {
+          caddr += kSlotW;
+        }
+      };
+      for (uint32_t it = 0; it < nmine; ++it) {
+        DL_PROF(2, 0);
+        uint64_t bd2[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bd2[j] = B2[j];
+        for (int jj = 0; jj < nk2; ++jj) {
+          c_take();
+          if (jj == nk2 - 1) {   // every D1(t) chunk has been read by CONV
+            if (elect_one()) mbar_arrive(&bars.s2_taken);
+            __syncwarp();
+          }
+          uint64_t bd[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] = bd2[j];
+          for (int oo = 0; oo < n2m; ++oo) {
+            if (elect_one()) kstep_ts<PARTS>(tD2 + (uint32_t)(oo * p.N2), caddr, 8, bd, id2, jj == 0);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] += o2s;
+          }
+          c_release(jj == nk2 - 1 ? &bars.d2_full : nullptr);
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd2[j] += ks2;
+        }
+        DL_PROF(2, 1);
+        uint64_t bg3[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bg3[j] = B3[j];
+        for (int o = 0; o < p.G2; ++o) {
+          if (n3 > 0) mbar_wait_warp(&bars.d3_free, (n3 - 1) & 1);
+          DL_PROF(2, 2 + 2 * o);
+          uint64_t bd[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] = bg3[j];
+          for (int jj = 0; jj < nk3; ++jj) {
+            c_take();
+            if (elect_one()) kstep_ts<PARTS>(tD3, caddr, 8, bd, id3, jj == 0);
+            __syncwarp();
+            c_release(jj == nk3 - 1 ? &bars.d3_full : nullptr);
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] += ks3;
+          }
+          ++n3;
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bg3[j] += g3s;
+          DL_PROF(2, 3 + 2 * o);
         }
       }
     }
