@@ -170,15 +170,20 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
 #ifndef DL_IDLE_MASK
 #define DL_IDLE_MASK 3   // bit 0: IN waits, bit 1: OUT waits
 #endif
+#ifndef DL_SUSPEND_NS
+#define DL_SUSPEND_NS 0
+#endif
 template <int ROLE>
 __device__ __forceinline__ void idle_wait(uint64_t* bar, uint32_t parity) {
-  if (DL_IDLE_NS > 0 && (DL_IDLE_MASK & (1 << ROLE))) mbar_wait_sleep(bar, parity, DL_IDLE_NS);
+  if (DL_SUSPEND_NS > 0) mbar_wait_suspend(bar, parity, DL_SUSPEND_NS);
+  else if (DL_IDLE_NS > 0 && (DL_IDLE_MASK & (1 << ROLE))) mbar_wait_sleep(bar, parity, DL_IDLE_NS);
   else mbar_wait_warp(bar, parity);
 }
 
-// wait used by the IN / CONV / OUT / loader roles (the MMA warp keeps mbar_wait_warp)
+// wait used by the IN / CONV / OUT / loader roles (the MMA warps keep mbar_wait_warp)
 __device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) {
-  if (kSleepNs) mbar_wait_sleep(bar, parity, kSleepNs);
+  if (DL_SUSPEND_NS > 0) mbar_wait_suspend(bar, parity, DL_SUSPEND_NS);
+  else if (kSleepNs) mbar_wait_sleep(bar, parity, kSleepNs);
   else mbar_wait_warp(bar, parity);
 }
 

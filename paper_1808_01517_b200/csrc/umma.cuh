@@ -178,6 +178,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Whole-warp wait with a suspend-time hint: the hardware may park the warp until the phase completes
+// (or the hint expires) instead of re-issuing the poll.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+  __syncwarp();
+}
+
 // mbar_wait by a whole warp, reconverged afterwards (lanes leave the polling loop independently, and
 // the .sync.aligned tcgen05 ops / elect.sync that follow need the full warp).
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
