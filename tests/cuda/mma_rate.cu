@@ -12,7 +12,8 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
   __shared__ uint64_t mbar;
   __shared__ uint32_t tb_s;
   const int warp = threadIdx.x / 32;
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  for (int i = threadIdx.x; i < (mode >= 70 ? 200 : 64) * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
   if (warp == 0) tmem_alloc(&tb_s, 512);
   if (threadIdx.x == 0) { mbar_init(&mbar, 1); mbar_fence_init(); }
   fence_proxy_async();
@@ -20,7 +21,96 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
   __syncthreads();
   fence_after();
   const uint32_t tb = tb_s;
-  if (mode >= 50) {
+  if (mode >= 70) {
+    // the chain kernel's stage-2 pattern: B = three 144x144 K-major images (SBO 2304) 41472 bytes apart
+    // in a 128 KB region, A alternating between two TMEM slots (cols 72 / 96), D at col 264 (N = 144),
+    // 9 K-steps per item, a commit per K-step.  mode 71: the B images one byte-offset 0 apart (same image)
+    __shared__ uint64_t mb2;
+    if (threadIdx.x == 0) { mbar_init(&mb2, 1); mbar_fence_init(); }
+    __syncthreads();
+    const uint32_t sb0 = smem_u32(smem);
+    const uint32_t id = idesc_bf16(128, 144, 0, 0);
+    if (warp == 0) {
+      const uint32_t img = mode == 71 ? 0u : 41472u;
+      long long t0 = clock64();
+      for (int it = 0; it < iters / 54; ++it) {
+        for (int jj = 0; jj < 9; ++jj) {
+          const uint32_t a0 = tb + ((jj & 1) ? 96u : 72u);
+          uint64_t bd[3];
+          for (int j = 0; j < 3; ++j) bd[j] = desc_noswz(sb0 + j * img + jj * 256, 128, 2304);
+          if (elect_one()) {
+            mma_ts(tb + 264, a0 + 16, bd[0], id, jj > 0);
+            mma_ts(tb + 264, a0 + 8, bd[1], id, 1);
+            mma_ts(tb + 264, a0, bd[2], id, 1);
+            mma_ts(tb + 264, a0 + 8, bd[0], id, 1);
+            mma_ts(tb + 264, a0, bd[1], id, 1);
+            mma_ts(tb + 264, a0, bd[0], id, 1);
+            commit(&mb2);
+          }
+          __syncwarp();
+        }
+      }
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+      mbar_wait(&mbar, 0);
+      long long t1 = clock64();
+      if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; }
+    }
+  } else if (mode >= 60) {
+    // issue cost under contention: warp 0 issues 6-MMA K-steps (N, TS) while warps 1..(blockDim/32-1)
+    // run an FMA/shared-memory busy loop.  mode 60: descriptors carried in registers (+= per step);
+    // mode 61: descriptors recomputed from the loop index inside the elected block.
+    __shared__ volatile int stop2;
+    if (threadIdx.x == 0) stop2 = 0;
+    __syncthreads();
+    const uint32_t sbb = smem_u32(smem + 32768);
+    const uint32_t id = idesc_bf16(128, N, 0, 0);
+    if (warp == 0) {
+      const uint64_t b0 = desc_noswz(sbb, 128, 256);
+      uint64_t bd[3] = {b0, b0 + 64, b0 + 128};
+      long long t0 = clock64();
+      for (int k = 0; k < iters / 6; ++k) {
+        if (mode == 60) {
+          if (elect_one()) {
+            mma_ts(tb + dcol, tb + acol + 16, bd[0], id, k > 0);
+            mma_ts(tb + dcol, tb + acol + 8, bd[1], id, 1);
+            mma_ts(tb + dcol, tb + acol, bd[2], id, 1);
+            mma_ts(tb + dcol, tb + acol + 8, bd[0], id, 1);
+            mma_ts(tb + dcol, tb + acol, bd[1], id, 1);
+            mma_ts(tb + dcol, tb + acol, bd[0], id, 1);
+          }
+          __syncwarp();
+          for (int j = 0; j < 3; ++j) bd[j] += ((k & 7) == 7) ? (uint64_t)-14 : 2;
+        } else {
+          if (elect_one()) {
+            const uint64_t kk = (uint64_t)(2 * (k & 7));
+            mma_ts(tb + dcol, tb + acol + 16, b0 + kk, id, k > 0);
+            mma_ts(tb + dcol, tb + acol + 8, b0 + 64 + kk, id, 1);
+            mma_ts(tb + dcol, tb + acol, b0 + 128 + kk, id, 1);
+            mma_ts(tb + dcol, tb + acol + 8, b0 + kk, id, 1);
+            mma_ts(tb + dcol, tb + acol, b0 + 64 + kk, id, 1);
+            mma_ts(tb + dcol, tb + acol, b0 + kk, id, 1);
+          }
+          __syncwarp();
+        }
+      }
+      if (elect_one()) commit(&mbar);
+      __syncwarp();
+      mbar_wait(&mbar, 0);
+      long long t1 = clock64();
+      if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; stop2 = 1; }
+    } else {
+      float a = threadIdx.x, b2 = 1.0001f;
+      volatile float* sm = reinterpret_cast<volatile float*>(smem);
+      long long n = 0;
+      while (!stop2) {
+        for (int r = 0; r < 32; ++r) a = a * b2 + 0.5f;
+        sm[(threadIdx.x * 4 + (int)n) & 4095] = a;
+        ++n;
+      }
+      if (a == 1.234f) out[1] = n;
+    }
+  } else if (mode >= 50) {
     // kernel-like B operand: K-major core-matrix image of N rows x Kc cols (SBO = Kc/8*128, LBO = 128),
     // 6 split-pair TS MMAs per K-step, K-step advance = 256 bytes; mode 51: MN-major (LBO = Nc/8*128, SBO = 128)
     const uint32_t sbb = smem_u32(smem);
@@ -195,8 +285,9 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
 extern "C" int mma_rate(int mode, int N, int iters, long long* out_host, int dcol, int acol) {
   long long* d;
   cudaMalloc(&d, 16);
-  cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  rate_k<<<1, mode >= 30 && mode < 40 ? 512 : 256, 64 * 1024>>>(mode, N, iters, d, dcol, acol);
+  cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int nthr = mode >= 60 ? 32 * (1 + (acol >> 16)) : (mode >= 30 && mode < 40 ? 512 : 256);
+  rate_k<<<1, nthr, mode >= 70 ? 200 * 1024 : 64 * 1024>>>(mode, N, iters, d, dcol, acol & 0xFFFF);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(out_host, d, 16, cudaMemcpyDeviceToHost);
   cudaFree(d);
