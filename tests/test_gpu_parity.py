@@ -435,3 +435,19 @@ def test_fused_chain_vs_oracle(dev, si, so, oi, oo, ni, no, grid, per_shell):
     assert rel(xt.grad, dx_ref) <= TOL_LSC
     assert rel(lsc.sconv.weight.grad[:, :, 0, :], dW_ref) <= TOL_LSC
     assert rel(lsc.sconv.bias.grad, db_ref) <= TOL_LSC
+
+
+@pytest.mark.parametrize("env", [{"DELIMIT_CHAIN_V2": "1"}, {"DELIMIT_NO_TMA": "1"},
+                                 {"DELIMIT_CHAIN_V2": "1", "DELIMIT_NO_TMA": "1"}])
+def test_fallback_kernels_match_oracle(env):
+    """The fallback device paths (compact-TMEM chain kernel, cp.async input rings instead of TMA) are
+    selected per shape at run time; force them process-wide and rerun the chain parity cases."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_parity.py"), "-q", "-x",
+                          "-m", "gpu", "-k", "fused_chain_vs_oracle or bitwise_deterministic"],
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=900, cwd=root)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
