@@ -700,9 +700,8 @@ struct Bars3v {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];
-  uint64_t d1_full, d2_full, d3_full, d3_free;
-  uint64_t d1_read;   // OUT has stored D1(t) to the mid buffer: the MMA may overwrite D1
-  uint64_t s2_taken;  // the stage-2/3 issuer holds every D1(t) conversion: D1 may be overwritten
+  uint64_t d1g_full[2], d1g_free[2];   // stage-1 accumulator, one input group at a time, two buffers
+  uint64_t d2_full, d3_full, d3_free;
   uint32_t tmem_base;
 };
 
@@ -744,12 +743,13 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       mbar_init(&bars.c_full[s], 4);   // one CONV warp per quadrant converts each item
       mbar_init(&bars.c_empty[s], 1);
     }
-    mbar_init(&bars.d1_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.d1g_full[b], 1);
+      mbar_init(&bars.d1g_free[b], kCV3);   // every CONV warp, once per group
+    }
     mbar_init(&bars.d2_full, 1);
     mbar_init(&bars.d3_full, 1);
     mbar_init(&bars.d3_free, kOUT3);
-    mbar_init(&bars.d1_read, kOUT3);
-    mbar_init(&bars.s2_taken, 1);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -779,56 +779,74 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     }
   } else if (warp < kIN3 + kCV3) {
     // =========================== CONV: accumulators -> conversion ring ===========================
-    // items per tile: nk2 D1 chunks (stage-2 A), then G2 x nk3 D2 chunks (+bias, stage-3 A); this warp
-    // converts items i = cw, cw + kCVQ, ... of the CTA-wide sequence (slot i % NAc)
+    // items per tile: for each input group g, n1c chunks of D1_g (stage-2 A, also stored to the mid
+    // buffer), then G2 x nk3 D2 chunks (+bias, stage-3 A).  Item i of the CTA-wide sequence belongs to
+    // CONV warp i % kCVQ and uses conversion slot i % NAc.
     const int cw = (warp - kIN3) >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
     const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
-    const int per_c = nk2 + p.G2 * nk3;
+    const int per_c = nk2 + p.G2 * nk3, n1c = p.N1 / 16;
     uint32_t cslot = (uint32_t)(cw % p.NAc), cround = (uint32_t)(cw / p.NAc), it = 0;
-    int i0 = cw;   // first item of this warp in the current tile
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    uint32_t base = 0;    // CTA-wide index of the tile's first item
+    uint32_t gq = 0;      // CTA-wide input-group counter (D1 buffer gq & 1)
+    auto put = [&](const uint32_t (&w)[PARTS][8]) {
+      if (cround > 0) role_wait(&bars.c_empty[cslot], (cround - 1) & 1);
+      fence_after();
+      store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
+      tmem_wait_st();
+      fence_before();
+      warp_arrive(&bars.c_full[cslot]);
+      cslot += kCVQ;
+      while (cslot >= (uint32_t)p.NAc) {
+        cslot -= p.NAc;
+        ++cround;
+      }
+    };
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it, base += (uint32_t)per_c) {
       const int64_t b = t / p.tiles_per_b, vx = (t - b * p.tiles_per_b) * kTileV + 32 * (warp & 3) + lane;
       const bool vok = vx < p.nvox;
+      uint16_t* mid = (p.mid && vx < p.mid_pitch)
+                          ? p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2) * 64 + (vx & 63)
+                          : nullptr;
       if (warp == kIN3) DL_PROF(1, 0);
-      role_wait(&bars.d1_full, it & 1);
-      if (warp == kIN3) DL_PROF(1, 1);
-      fence_after();
-      bool d2_seen = false;
-      int i = i0;
-      for (; i < per_c; i += kCVQ) {
-        float v[16];
-        if (i < nk2) {
-          ld16f(tq + p.colD1 + (uint32_t)i * 16, v);
-        } else {
-          if (!d2_seen) {
-            if (warp == kIN3) DL_PROF(1, 2);
-            role_wait(&bars.d2_full, it & 1);
-            if (warp == kIN3) DL_PROF(1, 3);
-            fence_after();
-            d2_seen = true;
-          }
-          const int o = (i - nk2) / nk3, j = (i - nk2) - o * nk3;
-          ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + 16 * j), v);
-          const float* bb = sb + o * p.N2 + 16 * j;
-#pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] += bb[e];
+      for (int g = 0; g < p.G1; ++g, ++gq) {
+        const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
+        role_wait(&bars.d1g_full[buf], (gq / nb) & 1);
+        fence_after();
+        for (int c = 0; c < n1c; ++c) {
+          const int i = g * n1c + c;
+          if ((base + (uint32_t)i) % kCVQ != (uint32_t)cw) continue;
+          float v[16];
+          ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
+          uint32_t w[PARTS][8];
+          split16<PARTS>(v, w);
+          if (mid)
+            store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
+          put(w);
         }
+        fence_before();
+        warp_arrive(&bars.d1g_free[buf]);   // this warp is done reading D1 buffer `buf`
+      }
+      if (warp == kIN3) DL_PROF(1, 2);
+      bool d2_seen = false;
+      for (int i = nk2; i < per_c; ++i) {
+        if ((base + (uint32_t)i) % kCVQ != (uint32_t)cw) continue;
+        if (!d2_seen) {
+          role_wait(&bars.d2_full, it & 1);
+          if (warp == kIN3) DL_PROF(1, 3);
+          fence_after();
+          d2_seen = true;
+        }
+        const int o = (i - nk2) / nk3, j = (i - nk2) - o * nk3;
+        float v[16];
+        ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + 16 * j), v);
+        const float* bb = sb + o * p.N2 + 16 * j;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] += bb[e];
         uint32_t w[PARTS][8];
         split16<PARTS>(v, w);
-        if (cround > 0) role_wait(&bars.c_empty[cslot], (cround - 1) & 1);
-        fence_after();
-        store_parts<PARTS>(tq + p.colC + cslot * kSlotW, 8, w);
-        tmem_wait_st();
-        fence_before();
-        warp_arrive(&bars.c_full[cslot]);
-        cslot += kCVQ;
-        while (cslot >= (uint32_t)p.NAc) {
-          cslot -= p.NAc;
-          ++cround;
-        }
+        put(w);
       }
-      i0 = i - per_c;   // items carry over tile boundaries when per_c is odd
     }
   } else if (warp < kW3MMA) {
     // =========================== OUT: D3 -> HBM ===========================
@@ -840,22 +858,6 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
-      // the stage-1 accumulator's first two split terms -> the tiled mid buffer (c for the Gram in the
-      // forward, g in the adjoint); OUT is otherwise idle while the conversions of stage 2 run
-      idle_wait<1>(&bars.d1_full, it & 1);
-      fence_after();
-      if (p.mid && v < p.mid_pitch) {
-        for (int ck = cg; ck < K2 / 16; ck += kOUTQ) {
-          float vv[16];
-          ld16f(tq + p.colD1 + (uint32_t)ck * 16, vv);
-          uint32_t w[2][8];
-          split16<2>(vv, w);
-          store_mid(p.mid + ((b * (p.mid_pitch >> 6) + (v >> 6)) * 2 * K2 + 16 * ck) * 64 + (v & 63), (int64_t)K2 * 64,
-                    64, w[0], w[1], vok ? p.mid_ones - 16 * ck : -1);
-        }
-      }
-      fence_before();
-      warp_arrive(&bars.d1_read);
       for (int o = 0; o < p.G2; ++o, ++n3) {
         idle_wait<1>(&bars.d3_full, n3 & 1);
         if (ow == 0) DL_PROF(1, 8 + 2 * o);
@@ -918,26 +920,26 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     uint32_t aaddr = tA, caddr = tC;
     const int n1 = p.G1 * nk1;
     if (warp == kW3MMA) {
-      // ---- stage 1: input chunks -> D1, tile after tile ----
+      // ---- stage 1: input chunks -> D1, one input group at a time into alternating buffers ----
+      uint32_t gq = 0;
       for (uint32_t it = 0; it < nmine; ++it) {
-        if (it > 0) {   // D1(t-1) fully converted (issuer 2 took every stage-2 item) and stored (OUT)
-          mbar_wait_warp(&bars.s2_taken, (it - 1) & 1);
-          mbar_wait_warp(&bars.d1_read, (it - 1) & 1);
-          fence_after();
-        }
-        uint32_t d1col = tD1;
-        for (int g = 0; g < p.G1; ++g, d1col += (uint32_t)p.N1) {
+        for (int g = 0; g < p.G1; ++g, ++gq) {
+          const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
+          if (gq >= nb) {   // CONV has read (and stored) the group that last used this buffer
+            mbar_wait_warp(&bars.d1g_free[buf], ((gq / nb) - 1) & 1);
+            fence_after();
+          }
+          const uint32_t d1col = tD1 + buf * (uint32_t)p.N1;
           uint64_t bd[PARTS];
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s;
           for (int k = 0; k < nk1; ++k) {
             mbar_wait_warp(&bars.a_full[aslot], around & 1);
             fence_after();
-            const bool last = k == nk1 - 1 && g == p.G1 - 1;
             if (elect_one()) {
               kstep_ts<PARTS>(d1col, aaddr, 8, bd, id1, k == 0);
               commit(&bars.a_empty[aslot]);
-              if (last) commit(&bars.d1_full);
+              if (k == nk1 - 1) commit(&bars.d1g_full[buf]);
             }
             __syncwarp();
             if (++aslot == (uint32_t)p.NA) {
@@ -979,10 +981,6 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         for (int j = 0; j < PARTS; ++j) bd2[j] = B2[j];
         for (int jj = 0; jj < nk2; ++jj) {
           c_take();
-          if (jj == nk2 - 1) {   // every D1(t) chunk has been read by CONV
-            if (elect_one()) mbar_arrive(&bars.s2_taken);
-            __syncwarp();
-          }
           uint64_t bd[PARTS];
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] = bd2[j];
@@ -1388,7 +1386,8 @@ bool plan_chain3(Chain3& p, int parts) {
 // chain3v: D1 | D2 | D3 resident, IN ring (NA) + conversion ring (NAc) in the remaining columns.
 bool plan_chain3v(Chain3& p, int parts) {
   if (p.N1 > 256 || p.N2 > 256 || p.N3 > 256 || p.G1 * p.N1 > 512) return false;
-  const int slotw = parts * 8, D1w = p.G1 * p.N1, D2w = p.G2 * p.N2, D3w = p.N3;
+  // stage 1 accumulates one input group at a time into two alternating N1-column buffers
+  const int slotw = parts * 8, D1w = (p.G1 >= 2 ? 2 : 1) * p.N1, D2w = p.G2 * p.N2, D3w = p.N3;
   const int nslots = (512 - D1w - D2w - D3w) / slotw;
   if (512 - D1w - D2w - D3w < 0 || nslots < 4) return false;
   // stage-1 input chunks are the most frequent handoff (18 per tile vs 9 + 9 conversions): IN gets the
