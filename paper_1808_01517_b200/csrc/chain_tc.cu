@@ -352,6 +352,58 @@ __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_
   }
 }
 
+// IN role, two chunks per TMEM item (one handoff per two K-steps): warp iw of a lane quadrant takes
+// the chunk pairs p = iw, iw + 2, ...; chunk q lives in ring stage q % NS (NS % 4 == 0: every stage
+// keeps one fixed consumer warp).  Pairs never straddle an input group (chunks per group is even).
+template <int PARTS, int NS, typename Geo>
+__device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
+                                             int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full,
+                                             uint64_t* a_empty, const float* ring, uint64_t* full, uint64_t* empty,
+                                             int iw) {
+  static_assert(NS % 4 == 0, "two-chunk IN items need NS % 4 == 0");
+  const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int odd0 = 8 * kBoxV + (int)(nvox & 3);
+  uint32_t aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
+  uint32_t pr = 0;   // CTA-wide pair index
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t b = t / tiles_per_b;
+    const bool vok = (t - b * tiles_per_b) * kTileV + 32 * qd + lane < nvox;
+    for (int r = 0; r < per_tile; r += 2, ++pr) {
+      if ((pr & 1u) != (uint32_t)iw) continue;
+      const uint32_t q0 = 2 * pr, cs0 = q0 % NS, cs1 = (q0 + 1) % NS;
+      const ChunkGeo cg = geo(r);
+      const int nval0 = vok ? cg.nval : 0, nval1 = vok ? cg.nval - 16 : 0;
+      float v0[16], v1[16];
+      idle_wait<0>(&full[cs0], (q0 / NS) & 1);
+      const float* rp0 = ring + cs0 * (kStageBytes / 4) + 32 * qd + lane;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v0[j] = j < nval0 ? rp0[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+      warp_arrive(&empty[cs0]);
+      idle_wait<0>(&full[cs1], ((q0 + 1) / NS) & 1);
+      const float* rp1 = ring + cs1 * (kStageBytes / 4) + 32 * qd + lane;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v1[j] = j < nval1 ? rp1[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+      warp_arrive(&empty[cs1]);
+      uint32_t w0[PARTS][8], w1[PARTS][8];
+      split16<PARTS>(v0, w0);
+      split16<PARTS>(v1, w1);
+      if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
+      fence_after();
+      const uint32_t ta = tslots + aslot * (2 * PARTS * 8);
+      store_parts<PARTS>(ta, 8, w0);
+      store_parts<PARTS>(ta + PARTS * 8, 8, w1);
+      tmem_wait_st();
+      fence_before();
+      warp_arrive(&a_full[aslot]);
+      aslot += 2;
+      while (aslot >= (uint32_t)NA) {
+        aslot -= NA;
+        ++around;
+      }
+    }
+  }
+}
+
 // ============================================================================ chain3 kernel
 struct Chain3 {
   CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
@@ -371,7 +423,9 @@ struct Chain3 {
   int C3, N3;                         // stage 3: real / padded out-ch per group
   int w1_groups, w3_groups;
   int adjoint, overlap, free_at, tma;
-  int NA, ns;                         // TMEM A slots, ring depth
+  int NA, ns;                         // TMEM A slots (IN items), ring depth
+  int cpi;                            // chain3v: input chunks per IN item (1 or 2; a 2-chunk item is one
+                                      // handoff for two K-steps)
   int NAc;                            // chain3v: conversion-ring slots
   uint32_t colC;                      // chain3v: conversion ring (A operands of stages 2 and 3)
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
@@ -768,7 +822,12 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
   if (warp < kIN3) {
     // =========================== IN ===========================
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
-    if (p.tma) {
+    if (p.tma && p.cpi == 2) {
+      if constexpr (NS % 4 == 0)
+        in_role_tma2<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full,
+                                bars.a_empty, reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty,
+                                warp >> 2);
+    } else if (p.tma) {
       in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
                              reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty, warp >> 2, 2);
     } else if (warp < 4) {
@@ -933,13 +992,19 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
           uint64_t bd[PARTS];
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s;
-          for (int k = 0; k < nk1; ++k) {
+          for (int k = 0; k < nk1; k += p.cpi) {   // one IN item = cpi K-steps
             mbar_wait_warp(&bars.a_full[aslot], around & 1);
             fence_after();
             if (elect_one()) {
               kstep_ts<PARTS>(d1col, aaddr, 8, bd, id1, k == 0);
+              if (p.cpi == 2) {
+                uint64_t bn[PARTS];
+#pragma unroll
+                for (int j = 0; j < PARTS; ++j) bn[j] = bd[j] + ks1;
+                kstep_ts<PARTS>(d1col, aaddr + kSlotW, 8, bn, id1, false);
+              }
               commit(&bars.a_empty[aslot]);
-              if (k == nk1 - 1) commit(&bars.d1g_full[buf]);
+              if (k + p.cpi >= nk1) commit(&bars.d1g_full[buf]);
             }
             __syncwarp();
             if (++aslot == (uint32_t)p.NA) {
@@ -947,10 +1012,10 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
               ++around;
               aaddr = tA;
             } else {
-              aaddr += kSlotW;
+              aaddr += (uint32_t)p.cpi * kSlotW;
             }
 #pragma unroll
-            for (int j = 0; j < PARTS; ++j) bd[j] += ks1;
+            for (int j = 0; j < PARTS; ++j) bd[j] += (uint64_t)p.cpi * ks1;
           }
         }
       }
@@ -1403,8 +1468,12 @@ bool plan_chain3v(Chain3& p, int parts) {
     p.NA = nslots - kCVQ;
   }
   if (p.NA < 2) return false;
+  // two input chunks per IN item halve the stage-1 handoffs: needs an even chunk count per group, the
+  // TMA path, and >= 2 double items (4 single slots)
+  p.cpi = (p.tma && (p.K1 / 16) % 2 == 0 && p.NA >= 4 && !getenv("DELIMIT_IN_SINGLE")) ? 2 : 1;
+  if (p.cpi == 2) p.NA /= 2;   // NA counts IN items from here on
   p.colA = 0;
-  p.colC = (uint32_t)(p.NA * slotw);
+  p.colC = (uint32_t)(p.NA * p.cpi * slotw);
   p.colD1 = p.colC + (uint32_t)(p.NAc * slotw);
   p.colD2 = p.colD1 + (uint32_t)D1w;
   p.colD3 = p.colD2 + (uint32_t)D2w;
@@ -1418,7 +1487,9 @@ bool plan_chain3v(Chain3& p, int parts) {
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N2 * 4, 128);
   p.sm_ring = (uint32_t)o;
   // even depths: two IN warps take alternate chunks, so each stage keeps one fixed consumer pair
+  // (two-chunk items: multiples of 4)
   for (int ns : {12, 10, 8, 6, 4, 2}) {
+    if (p.cpi == 2 && ns % 4) continue;
     p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
     p.sm_bar = (uint32_t)q;
