@@ -100,8 +100,12 @@ int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float
  * is not NULL the Signal2SH coefficients c = M x are also written there, as the backward's Gram
  * operand: an opaque buffer of dl_chain_mid_bytes(nbatch, s_in, r_in, nvox) bytes (16-byte aligned)
  * holding c's first two bf16 split terms per element (rows padded per shell to 16, voxels to 64).
- * Every product is an fp32-accurate split product (each fp32 operand as
- * DELIMIT_SPLIT_TERMS = 3 (default) or 2 bf16 terms, fp32 accumulation).
+ * Every product is an fp32-accurate split product with fp32 accumulation.  Default: each fp32 operand
+ * as two fp16 terms, activations scaled by a power of two (delayed scaling), then a 3-term bf16 pass
+ * that checks the recorded ranges and recomputes everything only when they were out of bounds.
+ * DELIMIT_SPLIT_TERMS=3 / 2 forces the 3-term / 2-term bf16 kernels alone.
+ * state: dl_chain_state_bytes() bytes of zero-initialised device memory the caller keeps between
+ * calls, one per direction and stream (the scale history); NULL runs the 3-term bf16 kernel only.
  * Backward: dy -> dx with the adjoint chain kernel, which also writes g = B'^T dy to g_mid
  * (dl_chain_mid_bytes(nbatch, s_out, r_out, nvox) bytes) when dW or db is requested; then the LSC
  * parameter gradient dW (s_out, s_in, K), db (s_out) from a streaming Gram kernel over
@@ -116,14 +120,16 @@ int dl_chain_split_terms(void);
 size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvox);
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);
+size_t dl_chain_state_bytes(void);
 int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
-                     const float* bvec, const float* Bt, void* workspace, int64_t nbatch, int64_t s_in,
-                     int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox,
-                     void* stream);
+                     const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch,
+                     int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                     int64_t nvox, void* stream);
 int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
                      const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
-                     const float* beta, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K,
-                     int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+                     const float* beta, void* workspace, void* state, int64_t nbatch, int64_t s_in,
+                     int64_t s_out, int64_t K, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                     int64_t nvox, void* stream);
 
 /* Number of kernel launches the last call on this host thread enqueued. */
 int dl_last_launch_count(void);

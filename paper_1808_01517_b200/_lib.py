@@ -36,8 +36,9 @@ SIGNATURES = {
     "dl_chain_split_terms": (_int, []),
     "dl_chain_mid_bytes": (_size, [_i64] * 4),
     "dl_chain_workspace_bytes": (_size, [_i64] * 8),
-    "dl_chain_fwd_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p, _c_p] + [_i64] * 8 + [_c_p]),
-    "dl_chain_bwd_f32": (_int, [_c_p] * 7 + [_int] + [_c_p] * 5 + [_i64] * 9 + [_c_p]),
+    "dl_chain_state_bytes": (_size, []),
+    "dl_chain_fwd_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p, _c_p, _c_p] + [_i64] * 8 + [_c_p]),
+    "dl_chain_bwd_f32": (_int, [_c_p] * 7 + [_int] + [_c_p] * 6 + [_i64] * 9 + [_c_p]),
     "dl_debug_chain_prof": (None, [_c_p]),
 }
 

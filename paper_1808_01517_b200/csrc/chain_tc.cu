@@ -26,6 +26,8 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "umma.cuh"
@@ -102,13 +104,15 @@ __device__ __forceinline__ void split_store16(uint32_t taddr_part0, uint32_t par
   for (int q = 0; q < PARTS; ++q) tmem_st<8>(taddr_part0 + (uint32_t)q * part_stride_cols, w[q]);
 }
 
-// split only (registers), so the TMEM slot can be awaited after the arithmetic
-template <int PARTS>
+// split only (registers), so the TMEM slot can be awaited after the arithmetic.  H: fp16 terms (the caller
+// scaled v by the launch's power of two), else bf16 terms.
+template <int PARTS, bool H = false>
 __device__ __forceinline__ void split16(const float (&v)[16], uint32_t (&w)[PARTS][8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     uint32_t pp[PARTS];
-    split_pair<PARTS>(v[2 * i], v[2 * i + 1], pp);
+    if constexpr (H) split_pair_h<PARTS>(v[2 * i], v[2 * i + 1], pp);
+    else split_pair<PARTS>(v[2 * i], v[2 * i + 1], pp);
 #pragma unroll
     for (int q = 0; q < PARTS; ++q) w[q][i] = pp[q];
   }
@@ -117,6 +121,26 @@ template <int PARTS>
 __device__ __forceinline__ void store_parts(uint32_t taddr_part0, uint32_t part_stride_cols, const uint32_t (&w)[PARTS][8]) {
 #pragma unroll
   for (int q = 0; q < PARTS; ++q) tmem_st<8>(taddr_part0 + (uint32_t)q * part_stride_cols, w[q]);
+}
+
+// Delayed scaling of the fp16 path: multiply by the launch's power of two and track the largest magnitude
+// (checked after the launch; NaN never raises it, inf does).
+template <bool H>
+__device__ __forceinline__ void scale16(float (&v)[16], float sc, float& amax) {
+  if constexpr (H) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] *= sc;
+      amax = fmaxf(amax, fabsf(v[i]));
+    }
+  }
+}
+template <bool H>
+__device__ __forceinline__ void track16(const float (&v)[16], float& amax) {
+  if constexpr (H) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  }
 }
 
 __device__ __forceinline__ void ld16f(uint32_t taddr, float (&v)[16]) {
@@ -214,11 +238,11 @@ __device__ __forceinline__ void stream_chunk(float* dst, const float* src, int64
 
 // Hands one voxel's 16 values (split into PARTS bf16 terms) to the MMA warp through TMEM A slot
 // (aslot, around), then advances the slot cursor by `step` chunks.
-template <int PARTS>
+template <int PARTS, bool H = false>
 __device__ __forceinline__ void put_a(const float (&v)[16], uint32_t tslots, int NA, uint64_t* a_full,
                                       uint64_t* a_empty, uint32_t& aslot, uint32_t& around, int step = 1) {
   uint32_t w[PARTS][8];
-  split16<PARTS>(v, w);
+  split16<PARTS, H>(v, w);
   if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
   fence_after();
   store_parts<PARTS>(tslots + aslot * (PARTS * 8), 8, w);
@@ -241,11 +265,13 @@ struct ChunkGeo {
 // Fallback IN role (no tensor map): each warp streams its own 32-voxel segment of its chunks
 // q = iw, iw + nIW, ... through a private NS-deep ring with 4-byte cp.async (any alignment).  Every
 // thread only reads back what it copied itself, so cp.async.wait_group is the only synchronisation.
-template <int PARTS, int NS, typename Geo>
+template <int PARTS, int NS, typename Geo, bool H = false>
 __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                                 int64_t nvox, const float* const (&base)[2], const int64_t (&bs)[2],
                                                 uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
-                                                float* ring, int iw = 0, int nIW = 1) {
+                                                float* ring, int iw = 0, int nIW = 1, float sc = 1.f,
+                                                float* amax = nullptr) {
+  float am = 0.f;
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int64_t nmine = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = nmine * per_tile;
@@ -276,9 +302,11 @@ __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, in
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = rp[r * 32];
     cslot = cslot + 1 == NS ? 0 : cslot + 1;
-    put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
+    scale16<H>(v, sc, am);
+    put_a<PARTS, H>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
   }
   cp_async_wait<0>();
+  if (H) *amax = fmaxf(*amax, am);
 }
 
 // TMA loader (one warp, one elected lane issues): chunk (tile, r) -> ring stage, as two 8 x 132 boxes of
@@ -319,11 +347,12 @@ __device__ __forceinline__ void tma_loader(const Geo& geo, int per_tile, int64_t
 
 // IN role over the TMA ring: thread = voxel; row j of the chunk is channel-pair row j/2 of box j%2.
 // This warp takes chunks q = iw, iw + nIW, ... (nIW a power of two).
-template <int PARTS, int NS, typename Geo>
+template <int PARTS, int NS, typename Geo, bool H = false>
 __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                             int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full, uint64_t* a_empty,
                                             const float* ring, uint64_t* full, uint64_t* empty, int iw = 0,
-                                            int nIW = 1) {
+                                            int nIW = 1, float sc = 1.f, float* amax = nullptr) {
+  float am = 0.f;
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int odd0 = 8 * kBoxV + (int)(nvox & 3);   // first odd-channel value of this thread, minus its voxel
   uint32_t s = 0, round = 0, aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
@@ -347,19 +376,22 @@ __device__ __forceinline__ void in_role_tma(const Geo& geo, int per_tile, int64_
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = j < nval ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
       warp_arrive(&empty[cs]);
-      put_a<PARTS>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
+      scale16<H>(v, sc, am);
+      put_a<PARTS, H>(v, tslots, NA, a_full, a_empty, aslot, around, nIW);
     }
   }
+  if (H) *amax = fmaxf(*amax, am);
 }
 
 // IN role, two chunks per TMEM item (one handoff per two K-steps): warp iw of a lane quadrant takes
 // the chunk pairs p = iw, iw + 2, ...; chunk q lives in ring stage q % NS (NS % 4 == 0: every stage
 // keeps one fixed consumer warp).  Pairs never straddle an input group (chunks per group is even).
-template <int PARTS, int NS, typename Geo>
+template <int PARTS, int NS, typename Geo, bool H = false>
 __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                              int64_t nvox, uint32_t tslots, int NA, uint64_t* a_full,
                                              uint64_t* a_empty, const float* ring, uint64_t* full, uint64_t* empty,
-                                             int iw) {
+                                             int iw, float sc = 1.f, float* amax = nullptr) {
+  float am = 0.f;
   static_assert(NS % 4 == 0, "two-chunk IN items need NS % 4 == 0");
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int odd0 = 8 * kBoxV + (int)(nvox & 3);
@@ -384,9 +416,11 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
 #pragma unroll
       for (int j = 0; j < 16; ++j) v1[j] = j < nval1 ? rp1[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
       warp_arrive(&empty[cs1]);
+      scale16<H>(v0, sc, am);
+      scale16<H>(v1, sc, am);
       uint32_t w0[PARTS][8], w1[PARTS][8];
-      split16<PARTS>(v0, w0);
-      split16<PARTS>(v1, w1);
+      split16<PARTS, H>(v0, w0);
+      split16<PARTS, H>(v1, w1);
       if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
       fence_after();
       const uint32_t ta = tslots + aslot * (2 * PARTS * 8);
@@ -402,6 +436,7 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
       }
     }
   }
+  if (H) *amax = fmaxf(*amax, am);
 }
 
 // ============================================================================ chain3 kernel
@@ -432,7 +467,60 @@ struct Chain3 {
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
   uint32_t colA, colD1, colA2, colD2, colA3, colD3;
   long long* prof;                    // debug: per-role phase timestamps of CTA 0 (dl_debug_chain_prof)
+  uint32_t* rstate;                   // chain3v delayed-scaling state (kState* words) or null
+  int redo;                           // chain3v bf16 pass: check the fp16 pass's ranges, recompute if needed
 };
+
+// Delayed scaling of the fp16 chain (state words, caller-owned, zero-initialised):
+//   the fp16 pass multiplies its input by 2^exp, records the largest scaled input magnitude (amax_in) and
+//   the largest scaled accumulator it converts (amax_mid); the bf16 pass launched right after checks them:
+//   in range -> every CTA exits at once; out of range -> it recomputes everything with 3-term bf16 operands
+//   (no range limits).  Its last CTA re-centres exp on the measured magnitudes and clears the words.
+enum : int { kStExp = 0, kStAmaxIn, kStAmaxMid, kStArrive, kStRedos, kStChecks, kStateWords = 8 };
+__device__ __forceinline__ bool range_ok(float ai, float am) {
+  // fp16: max 65504, 2^-24 subnormal spacing.  ai >= 2^-2 keeps the absolute rounding floor (2^-25) below
+  // 2^-23 of the largest input; <= 2^14 leaves headroom for the split terms and the accumulators.
+  return ai >= 0.25f && ai <= 16384.f && am <= 16384.f;
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// the check of the bf16 pass (thread 0 of each CTA); true: the fp16 pass's results stand
+__device__ __forceinline__ bool range_check(uint32_t* st) {
+  volatile uint32_t* v = st;
+  const float ai = __uint_as_float(v[kStAmaxIn]), am = __uint_as_float(v[kStAmaxMid]);
+  const bool ok = range_ok(ai, am);
+  __threadfence();
+  if (atomicAdd(st + kStArrive, 1u) == gridDim.x - 1) {   // last CTA: every CTA has read the verdict
+    __threadfence();
+    int e = (int)v[kStExp];
+    if (ai > 0.f && ai <= 3.0e38f) {   // re-centre: largest input near 2^8, accumulators below 2^12
+      int k;
+      frexpf(ai, &k);                  // ai in [2^(k-1), 2^k)
+      int d = 8 - k;
+      if (am > 0.f && am <= 3.0e38f) {
+        int km;
+        frexpf(am, &km);
+        if (km + d > 12) d = 12 - km;
+      }
+      e += d;
+      e = e < -100 ? -100 : e > 100 ? 100 : e;
+    }
+    v[kStExp] = (uint32_t)e;
+    v[kStAmaxIn] = 0u;
+    v[kStAmaxMid] = 0u;
+    v[kStArrive] = 0u;
+    if (!ok) v[kStRedos] = v[kStRedos] + 1u;
+    v[kStChecks] = v[kStChecks] + 1u;
+    __threadfence();
+  }
+  return ok;
+}
+
+__device__ __forceinline__ void amax_publish(uint32_t* word, float am) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(word, __float_as_uint(am));
+}
 
 // role r (0 IN, 1 MID, 2 MMA, 3 loader), tile it < 8, event ev < 32
 #define DL_PROF(r, ev)                                                                   \
@@ -759,13 +847,25 @@ struct Bars3v {
   uint32_t tmem_base;
 };
 
-template <int PARTS, int NS>
+// H: fp16 two-term operands under delayed scaling (p.rstate), else bf16 PARTS-term operands.
+template <int PARTS, int NS, bool H>
 __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant__ Chain3 p) {
   static_assert(NS % 2 == 0, "two IN warps alternate chunks: each ring stage needs one fixed consumer pair");
+  static_assert(!H || PARTS == 2, "the fp16 path uses two terms");
   extern __shared__ __align__(1024) uint8_t smem[];
+  if (!H && p.redo) {
+    if (__syncthreads_or(threadIdx.x == 0 ? (range_check(p.rstate) ? 1 : 0) : 0)) return;
+  }
   Bars3v& bars = *reinterpret_cast<Bars3v*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kSlotW = PARTS * 8;
+  int sexp = 0;
+  if constexpr (H) {
+    sexp = (int)*(volatile const uint32_t*)(p.rstate + kStExp);
+    sexp = sexp < -100 ? -100 : sexp > 100 ? 100 : sexp;
+  }
+  const float sc = pow2f(sexp), isc = pow2f(-sexp);   // 1 on the bf16 path
+  float amax = 0.f;                                   // IN: scaled inputs; CONV: scaled accumulators
 
   {  // stage weight images + bias once per CTA
     const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = (uint32_t)PARTS * p.w2_img,
@@ -780,7 +880,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     float* sb = reinterpret_cast<float*>(smem + p.sm_bias);
     for (int i = threadIdx.x; i < p.G2 * p.N2; i += blockDim.x) {
       const int o = i / p.N2, r = i - o * p.N2;
-      sb[i] = (p.bias2 && r < p.C2) ? __ldg(p.bias2 + o * p.C2 + r) : 0.f;
+      sb[i] = (p.bias2 && r < p.C2) ? __ldg(p.bias2 + o * p.C2 + r) * sc : 0.f;
     }
   }
   if (warp == kW3MMA) tmem_alloc(&bars.tmem_base, 512);
@@ -824,18 +924,24 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
     if (p.tma && p.cpi == 2) {
       if constexpr (NS % 4 == 0)
-        in_role_tma2<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full,
-                                bars.a_empty, reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty,
-                                warp >> 2);
+        in_role_tma2<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
+                                                  bars.a_full, bars.a_empty,
+                                                  reinterpret_cast<const float*>(smem + p.sm_ring), bars.full,
+                                                  bars.empty, warp >> 2, sc, &amax);
     } else if (p.tma) {
-      in_role_tma<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA, bars.a_full, bars.a_empty,
-                             reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty, warp >> 2, 2);
+      in_role_tma<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
+                                               bars.a_full, bars.a_empty,
+                                               reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty,
+                                               warp >> 2, 2, sc, &amax);
     } else if (warp < 4) {
       const float* const base[2] = {p.in, p.in};
       const int64_t bs[2] = {p.in_bs, p.in_bs};
-      in_role_cpasync<PARTS, NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots, p.NA, bars.a_full,
-                                 bars.a_empty, reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
+      in_role_cpasync<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots,
+                                                   p.NA, bars.a_full, bars.a_empty,
+                                                   reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512, 0, 1,
+                                                   sc, &amax);
     }
+    if (H) amax_publish(p.rstate + kStAmaxIn, amax);
   } else if (warp < kIN3 + kCV3) {
     // =========================== CONV: accumulators -> conversion ring ===========================
     // items per tile: for each input group g, n1c chunks of D1_g (stage-2 A, also stored to the mid
@@ -877,10 +983,21 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
           if ((base + (uint32_t)i) % kCVQ != (uint32_t)cw) continue;
           float v[16];
           ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
+          track16<H>(v, amax);
           uint32_t w[PARTS][8];
-          split16<PARTS>(v, w);
-          if (mid)
-            store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
+          split16<PARTS, H>(v, w);
+          if (mid) {
+            if constexpr (H) {   // the Gram operand is unscaled bf16 (hi, next term)
+              float u[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
+              uint32_t m[2][8];
+              split16<2>(u, m);
+              store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
+            } else {
+              store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
+            }
+          }
           put(w);
         }
         fence_before();
@@ -902,11 +1019,13 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         const float* bb = sb + o * p.N2 + 16 * j;
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] += bb[e];
+        track16<H>(v, amax);
         uint32_t w[PARTS][8];
-        split16<PARTS>(v, w);
+        split16<PARTS, H>(v, w);
         put(w);
       }
     }
+    if (H) amax_publish(p.rstate + kStAmaxMid, amax);
   } else if (warp < kW3MMA) {
     // =========================== OUT: D3 -> HBM ===========================
     const int ow = warp - kIN3 - kCV3, qd = warp & 3, cg = ow >> 2;
@@ -924,6 +1043,10 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         for (int ck = cg; ck < p.N3 / 16; ck += kOUTQ) {
           float vv[16];
           ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
+          if constexpr (H) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vv[e] *= isc;
+          }
           if (vok) {
             float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             const int nval = p.C3 - ck * 16;
@@ -957,9 +1080,10 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     const int km = p.adjoint ? 0 : 1;
     const int NT2 = p.G2 * p.N2;
     const int n2m = NT2 <= 256 ? 1 : p.G2;   // stage-2 MMAs per item (N split when > 256)
-    const uint32_t id1 = idesc_bf16(128, p.N1, 0, 1 - km);
-    const uint32_t id2 = idesc_bf16(128, n2m == 1 ? NT2 : p.N2, 0, 1 - km);
-    const uint32_t id3 = idesc_bf16(128, p.N3, 0, 1 - km);
+    const uint32_t id1 = H ? idesc_f16(128, p.N1, 0, 1 - km) : idesc_bf16(128, p.N1, 0, 1 - km);
+    const uint32_t id2 = H ? idesc_f16(128, n2m == 1 ? NT2 : p.N2, 0, 1 - km)
+                           : idesc_bf16(128, n2m == 1 ? NT2 : p.N2, 0, 1 - km);
+    const uint32_t id3 = H ? idesc_f16(128, p.N3, 0, 1 - km) : idesc_bf16(128, p.N3, 0, 1 - km);
     const int c1 = km ? p.K1 : p.N1, c2 = km ? K2 : NT2, c3 = km ? p.N2 : p.N3;
     const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(c2, km), ks3 = wkstep(c3, km);
     uint64_t B1[PARTS], B2[PARTS], B3[PARTS];
@@ -1251,8 +1375,9 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
 // ---------------------------------------------------------------------------- operand packing
 // `ng` row-major fp32 matrices of (nrb*rb) x (ncb*cb) -> PARTS bf16 images each of (nrb*rbp) x (ncb*cbp)
 // in the core-matrix blocked layout, image (q, g) at (q * ng + g) * img_elems.  Padding is zero.
-__global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, int ng, int nrb, int rb, int rbp,
-                       int ncb, int cb, int cbp, int parts) {
+// out_h (optional): the same images as two fp16 terms (the fp16 chain pass).
+__global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, uint16_t* __restrict__ out_h, int ng,
+                       int nrb, int rb, int rbp, int ncb, int cb, int cbp, int parts) {
   const int R = nrb * rbp, C = ncb * cbp;
   const int64_t img = (int64_t)R * C;
   const int64_t n = img * ng;
@@ -1265,6 +1390,14 @@ __global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, 
     if (rr < rb && cc < cb)
       v = __ldg(W + (int64_t)g * (nrb * rb) * (ncb * cb) + (int64_t)(bi * rb + rr) * (ncb * cb) + bj * cb + cc);
     const int64_t off = ((int64_t)(r >> 3) * (C >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+    if (out_h) {
+      float u = v;
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t pk = pack_f16x2(u, 0.f);
+        out_h[((int64_t)q * ng + g) * img + off] = (uint16_t)(pk & 0xFFFFu);
+        u -= f16lo_to_f32(pk);
+      }
+    }
     for (int q = 0; q < parts; ++q) {
       const uint32_t pk = pack_bf16x2(v, 0.f);
       out[((int64_t)q * ng + g) * img + off] = (uint16_t)(pk & 0xFFFFu);
@@ -1333,12 +1466,19 @@ constexpr int kMaxParts = 256;
 
 long long* g_prof = nullptr;   // debug: phase timestamps of the next chain3 forward launch
 
+// Operand precision of the chain kernels (DELIMIT_SPLIT_TERMS): unset (default) = fp16 two-term pass under
+// delayed scaling, checked and if needed redone by a 3-term bf16 pass; "3" = 3-term bf16 only; "2" = 2-term
+// bf16 only (~3e-5 relative error, below the fp32-class bar; a measurement mode).
 int split_terms() {
   static int v = [] {
     const char* e = getenv("DELIMIT_SPLIT_TERMS");
     const int t = e ? atoi(e) : 3;
     return (t == 2 || t == 3) ? t : 3;
   }();
+  return v;
+}
+bool fp16_pass() {
+  static const bool v = getenv("DELIMIT_SPLIT_TERMS") == nullptr;
   return v;
 }
 
@@ -1369,7 +1509,7 @@ Dims make_dims(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r
 }
 
 struct WsLayout {
-  size_t imgM, imgL, imgB, parts, G, total;
+  size_t imgM, imgL, imgB, imgMh, imgLh, imgBh, parts, G, total;
 };
 
 WsLayout ws_layout(const Dims& d, int nparts) {
@@ -1381,6 +1521,9 @@ WsLayout ws_layout(const Dims& d, int nparts) {
   w.imgM = o; o = al(o + 3 * d.mg * bM, 256);
   w.imgL = o; o = al(o + 3 * bL, 256);
   w.imgB = o; o = al(o + 3 * bB, 256);
+  w.imgMh = o; o = al(o + 2 * d.mg * bM, 256);   // fp16 two-term images
+  w.imgLh = o; o = al(o + 2 * bL, 256);
+  w.imgBh = o; o = al(o + 2 * bB, 256);
   w.parts = o; o = al(o + (size_t)nparts * (GR * GC + d.s_out) * 4, 256);
   w.G = o; o = al(o + GR * GC * 8, 256);
   w.total = o;
@@ -1535,29 +1678,47 @@ int run_chain3(const Chain3& p, int grid, cudaStream_t st) {
   return after_launch("chain3_tc");
 }
 
-template <int PARTS, int NS>
+template <int PARTS, int NS, bool H>
 int launch_chain3v(const Chain3& p, int grid, cudaStream_t st) {
-  DL_CUDA(cudaFuncSetAttribute(chain3v_tc<PARTS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
-  chain3v_tc<PARTS, NS><<<grid, kThreads3, p.smem_bytes, st>>>(p);
-  return after_launch("chain3v_tc");
+  DL_CUDA(cudaFuncSetAttribute(chain3v_tc<PARTS, NS, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)p.smem_bytes));
+  chain3v_tc<PARTS, NS, H><<<grid, kThreads3, p.smem_bytes, st>>>(p);
+  return after_launch(H ? "chain3v_tc(fp16)" : "chain3v_tc");
 }
 
-template <int PARTS>
+template <int PARTS, bool H = false>
 int run_chain3v(const Chain3& p, int grid, cudaStream_t st) {
   switch (p.ns) {
-    case 2: return launch_chain3v<PARTS, 2>(p, grid, st);
-    case 4: return launch_chain3v<PARTS, 4>(p, grid, st);
-    case 6: return launch_chain3v<PARTS, 6>(p, grid, st);
-    case 8: return launch_chain3v<PARTS, 8>(p, grid, st);
-    case 10: return launch_chain3v<PARTS, 10>(p, grid, st);
-    default: return launch_chain3v<PARTS, 12>(p, grid, st);
+    case 2: return launch_chain3v<PARTS, 2, H>(p, grid, st);
+    case 4: return launch_chain3v<PARTS, 4, H>(p, grid, st);
+    case 6: return launch_chain3v<PARTS, 6, H>(p, grid, st);
+    case 8: return launch_chain3v<PARTS, 8, H>(p, grid, st);
+    case 10: return launch_chain3v<PARTS, 10, H>(p, grid, st);
+    default: return launch_chain3v<PARTS, 12, H>(p, grid, st);
   }
 }
 
-// plan + launch one chain3 direction on the best kernel that fits
-int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* what) {
+// plan + launch one chain3 direction on the best kernel that fits.  With a delayed-scaling state (and the
+// default precision mode): the fp16 pass, then the bf16 pass that checks it and recomputes only if needed.
+// p's images are the bf16 ones; hw1/hw2/hw3 the fp16 images.
+int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* what, uint32_t* rstate = nullptr,
+              const uint16_t* hw1 = nullptr, const uint16_t* hw2 = nullptr, const uint16_t* hw3 = nullptr) {
   Chain3 v = p;
-  if (use_v3() && plan_chain3v(v, d.parts)) return d.parts == 3 ? run_chain3v<3>(v, grid, st) : run_chain3v<2>(v, grid, st);
+  if (use_v3() && plan_chain3v(v, d.parts)) {
+    Chain3 h = p;
+    if (rstate && d.parts == 3 && hw1 && plan_chain3v(h, 2)) {
+      h.w1 = hw1;
+      h.w2 = hw2;
+      h.w3 = hw3;
+      h.rstate = rstate;
+      h.redo = 0;
+      DL_TRY((run_chain3v<2, true>(h, grid, st)));
+      v.rstate = rstate;
+      v.redo = 1;
+      v.prof = nullptr;
+    }
+    return d.parts == 3 ? run_chain3v<3>(v, grid, st) : run_chain3v<2>(v, grid, st);
+  }
   if (!plan_chain3(p, d.parts)) return dl::fail(DL_EINVAL, "%s: channel counts exceed the fused kernel's plan", what);
   return d.parts == 3 ? run_chain3<3>(p, grid, st) : run_chain3<2>(p, grid, st);
 }
@@ -1577,27 +1738,39 @@ int run_gram(const GramP& p, int grid, cudaStream_t st) {
   }
 }
 
-int pack(const float* W, uint16_t* out, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp, int parts,
-         cudaStream_t st) {
+int pack(const float* W, uint16_t* out, uint16_t* out_h, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp,
+         int parts, cudaStream_t st) {
   const int64_t n = (int64_t)ng * nrb * rbp * ncb * cbp;
   const int blocks = (int)((n + 255) / 256 < 2048 ? (n + 255) / 256 : 2048);
-  pack_k<<<blocks, 256, 0, st>>>(W, out, ng, nrb, rb, rbp, ncb, cb, cbp, parts);
+  pack_k<<<blocks, 256, 0, st>>>(W, out, out_h, ng, nrb, rb, rbp, ncb, cb, cbp, parts);
   return after_launch("pack_operand");
 }
 
-int pack_all(const Dims& d, const WsLayout& w, uint8_t* ws, const float* M, const float* L, const float* Bt,
+// bf16 images (d.parts terms) and, for the fp16 pass, the fp16 two-term images
+int pack_all(const Dims& d, const WsLayout& w, uint8_t* ws, const float* M, const float* L, const float* Bt, bool h,
              cudaStream_t st) {
-  if (M) DL_TRY(pack(M, reinterpret_cast<uint16_t*>(ws + w.imgM), d.mg, 1, d.r_in, d.RPi, 1, d.n, d.NPi, d.parts, st));
-  if (L)
-    DL_TRY(pack(L, reinterpret_cast<uint16_t*>(ws + w.imgL), 1, d.s_out, d.r_out, d.RPo, d.s_in, d.r_in, d.RPi,
-                d.parts, st));
-  if (Bt)
-    DL_TRY(pack(Bt, reinterpret_cast<uint16_t*>(ws + w.imgB), 1, 1, d.n_out, d.NPo, 1, d.r_out, d.RPo, d.parts, st));
+  auto img = [&](size_t off, size_t off_h) {
+    return std::make_pair(reinterpret_cast<uint16_t*>(ws + off), h ? reinterpret_cast<uint16_t*>(ws + off_h) : nullptr);
+  };
+  if (M) {
+    auto [o, oh] = img(w.imgM, w.imgMh);
+    DL_TRY(pack(M, o, oh, d.mg, 1, d.r_in, d.RPi, 1, d.n, d.NPi, d.parts, st));
+  }
+  if (L) {
+    auto [o, oh] = img(w.imgL, w.imgLh);
+    DL_TRY(pack(L, o, oh, 1, d.s_out, d.r_out, d.RPo, d.s_in, d.r_in, d.RPi, d.parts, st));
+  }
+  if (Bt) {
+    auto [o, oh] = img(w.imgB, w.imgBh);
+    DL_TRY(pack(Bt, o, oh, 1, 1, d.n_out, d.NPo, 1, d.r_out, d.RPo, d.parts, st));
+  }
   return DL_OK;
 }
 
 Chain3 chain3_params(const Dims& d, const WsLayout& w, const uint8_t* ws, bool adjoint) {
   Chain3 p{};
+  p.redo = 0;
+  p.rstate = nullptr;
   p.nbatch = d.nbatch;
   p.nvox = d.nvox;
   p.tiles_per_b = (d.nvox + kTileV - 1) / kTileV;
@@ -1732,6 +1905,8 @@ int dl_chain_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int
 
 int dl_chain_split_terms(void) { return dl::tc::split_terms(); }
 
+size_t dl_chain_state_bytes(void) { return dl::tc::kStateWords * sizeof(uint32_t); }
+
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out,
                                 int64_t n_out, int64_t nvox) {
   using namespace dl::tc;
@@ -1744,8 +1919,8 @@ size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvo
 }
 
 int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
-                     const float* bvec, const float* Bt, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out,
-                     int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+                     const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch, int64_t s_in,
+                     int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   using namespace dl::tc;
   dl::begin_call();
   int sm = 0;
@@ -1760,7 +1935,8 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   DL_REQUIRE(chain_fits(d), "chain_fwd: channel counts exceed the fused kernel's TMEM/smem plan");
   if (nbatch == 0 || nvox == 0) return DL_OK;
   cudaStream_t st = dl::as_stream(stream);
-  DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
+  const bool h = state && fp16_pass();
+  DL_TRY(pack_all(d, w, ws, M, L, Bt, h, st));
   p.in = x;
   p.out = y;
   p.mid = reinterpret_cast<uint16_t*>(c_mid);
@@ -1771,13 +1947,15 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   p.prof = g_prof;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
-  return run_chain(p, d, grid, st, "chain_fwd");
+  return run_chain(p, d, grid, st, "chain_fwd", h ? reinterpret_cast<uint32_t*>(state) : nullptr,
+                   reinterpret_cast<const uint16_t*>(ws + w.imgMh), reinterpret_cast<const uint16_t*>(ws + w.imgLh),
+                   reinterpret_cast<const uint16_t*>(ws + w.imgBh));
 }
 
 int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
                      const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
-                     const float* beta, void* workspace, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K,
-                     int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+                     const float* beta, void* workspace, void* state, int64_t nbatch, int64_t s_in, int64_t s_out,
+                     int64_t K, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   using namespace dl::tc;
   dl::begin_call();
   int sm = 0;
@@ -1791,7 +1969,8 @@ int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, f
   cudaStream_t st = dl::as_stream(stream);
   const int64_t ntiles = nbatch * ((nvox + kTileV - 1) / kTileV);
   const bool wgrad = dW || db;
-  DL_TRY(pack_all(d, w, ws, M, L, Bt, st));
+  const bool h = state && fp16_pass();
+  DL_TRY(pack_all(d, w, ws, M, L, Bt, h, st));
   if (ntiles > 0) {
     // adjoint chain dy -> dx; its stage-1 accumulator g = B'^T dy goes to g_mid for the Gram
     Chain3 p = chain3_params(d, w, ws, true);
@@ -1803,7 +1982,10 @@ int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, f
     p.mid_ones = -1;
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
-    DL_TRY(run_chain(p, d, grid_for(ntiles, sm), st, "chain_bwd"));
+    // adjoint: stage 1 uses B' (w1 = imgB), stage 3 uses M (w3 = imgM)
+    DL_TRY(run_chain(p, d, grid_for(ntiles, sm), st, "chain_bwd", h ? reinterpret_cast<uint32_t*>(state) : nullptr,
+                     reinterpret_cast<const uint16_t*>(ws + w.imgBh), reinterpret_cast<const uint16_t*>(ws + w.imgLh),
+                     reinterpret_cast<const uint16_t*>(ws + w.imgMh)));
   }
   if (wgrad) {
     GramP g = gram_params(d, w, ws);

@@ -52,6 +52,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
        | ((uint32_t)(N >> 3) << 17)
        | ((uint32_t)(M >> 4) << 24);
 }
+// Same for fp16 x fp16 -> f32 (A / B format fields 0 = F16).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                      // D format F32
+       | ((uint32_t)a_mn_major << 15)
+       | ((uint32_t)b_mn_major << 16)
+       | ((uint32_t)(N >> 3) << 17)
+       | ((uint32_t)(M >> 4) << 24);
+}
 
 // 1 on exactly one lane of a converged warp (elect.sync).
 __device__ __forceinline__ uint32_t elect_one() {
@@ -299,6 +307,38 @@ __device__ __forceinline__ void split_pair(float a, float b, uint32_t (&part)[NP
     if (i + 1 < NP) {   // the last residual is never used
       a -= bf16lo_to_f32(p);
       b -= bf16hi_to_f32(p);
+    }
+  }
+}
+
+// Round-to-nearest fp16 pair of (a, b) packed as (lo16 = a, hi16 = b).
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;\n" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f16lo_to_f32(uint32_t p) {
+  float f;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tcvt.f32.f16 %0, lo;\n\t}\n" : "=f"(f) : "r"(p));
+  return f;
+}
+__device__ __forceinline__ float f16hi_to_f32(uint32_t p) {
+  float f;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tcvt.f32.f16 %0, hi;\n\t}\n" : "=f"(f) : "r"(p));
+  return f;
+}
+
+// Split (a, b) into NP fp16 parts (same packing as split_pair).  The caller scales the operands so the
+// largest magnitude sits well inside the fp16 range (delayed scaling in chain3v_tc).
+template <int NP>
+__device__ __forceinline__ void split_pair_h(float a, float b, uint32_t (&part)[NP]) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const uint32_t p = pack_f16x2(a, b);
+    part[i] = p;
+    if (i + 1 < NP) {
+      a -= f16lo_to_f32(p);
+      b -= f16hi_to_f32(p);
     }
   }
 }

@@ -216,6 +216,14 @@ class SphericalChain(nn.Module):
             raise ShapeError(f"Signal2SH has {len(s2sh.operators)} shell operators, LSC expects {lsc.shells_in}")
         self.s2sh, self.lsc, self.sh2s = s2sh, lsc, sh2s
         self._fused = None
+        self._state = {}   # device -> (forward, adjoint) delayed-scaling state of the fp16 chain pass
+
+    def range_state(self, device):
+        """The (forward, adjoint) scale-history tensors of the fused kernels on `device` (ops.chain_state)."""
+        key = str(device)
+        if key not in self._state:
+            self._state[key] = (ops.chain_state(device), ops.chain_state(device))
+        return self._state[key]
 
     def fused(self) -> bool:
         if self._fused is None:
@@ -236,6 +244,7 @@ class SphericalChain(nn.Module):
         w = self.lsc.sconv.weight
         w3 = w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous()
         b = self.lsc.sconv.bias
+        sf, sb = self.range_state(x.device)
         return ops.ChainFunction.apply(x, w3, None if b is None else b.float().contiguous(),
                                        self.s2sh.fit_matrix, self.s2sh.per_shell, self.lsc.fold, self.lsc.beta,
-                                       self.sh2s.basis)
+                                       self.sh2s.basis, sf, sb)

@@ -158,7 +158,7 @@ class ChainFunction(torch.autograd.Function):
     """
 
     @staticmethod
-    def forward(ctx, x, weight, bias, M, per_shell, fold, beta, Bt):
+    def forward(ctx, x, weight, bias, M, per_shell, fold, beta, Bt, state_fwd=None, state_bwd=None):
         s_out, s_in = weight.shape[0], weight.shape[1]
         K, r_out, r_in = fold.shape
         n = M.shape[-1]
@@ -171,8 +171,9 @@ class ChainFunction(torch.autograd.Function):
         c_mid = _workspace(lib.dl_chain_mid_bytes(B, s_in, r_in, V), x.device) if want_w else None
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
         _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(c_mid), _p(M), int(per_shell), _p(L), _p(bvec), _p(Bt),
-                  _p(ws), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
+                  _p(ws), _p(state_fwd), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
         ctx.save_for_backward(c_mid, weight, M, fold, beta, Bt, L)
+        ctx.state_bwd = state_bwd
         ctx.per_shell = per_shell
         ctx.has_bias = bias is not None
         ctx.shape = (B, V, tuple(x.shape))
@@ -191,7 +192,7 @@ class ChainFunction(torch.autograd.Function):
         want_w = ctx.needs_input_grad[1] and c_mid is not None
         want_b = ctx.has_bias and ctx.needs_input_grad[2] and c_mid is not None
         if not (want_x or want_w or want_b):
-            return None, None, None, None, None, None, None, None
+            return (None,) * 10
         lib = _lib.load()
         # the adjoint kernel always runs (it produces g for the Gram); dx is discarded if not wanted
         dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
@@ -200,11 +201,23 @@ class ChainFunction(torch.autograd.Function):
         g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device) if (want_w or want_b) else None
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
         _lib.call("dl_chain_bwd_f32", _p(c_mid), _p(dy), _p(dx), _p(dW), _p(db), _p(g_mid), _p(M),
-                  int(ctx.per_shell), _p(L), _p(Bt), _p(fold), _p(beta), _p(ws), B, s_in, s_out, K, n, r_in, r_out,
-                  n_out, V, _stream())
+                  int(ctx.per_shell), _p(L), _p(Bt), _p(fold), _p(beta), _p(ws), _p(ctx.state_bwd), B, s_in, s_out, K,
+                  n, r_in, r_out, n_out, V, _stream())
         if dW is not None:
             dW = dW.view(weight.shape)
-        return (dx if want_x else None), dW, db, None, None, None, None, None
+        return (dx if want_x else None), dW, db, None, None, None, None, None, None, None
+
+
+def chain_state(device) -> torch.Tensor:
+    """Zeroed delayed-scaling state for one chain direction (dl_chain_state_bytes; kept across calls)."""
+    return torch.zeros(int(_lib.load().dl_chain_state_bytes()) // 4, dtype=torch.int32, device=device)
+
+
+def fp16_pass_enabled() -> bool:
+    """True when the fused chain runs the fp16 two-term pass (the default precision mode)."""
+    import os
+
+    return "DELIMIT_SPLIT_TERMS" not in os.environ
 
 
 def chain_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int, per_shell: bool) -> bool:

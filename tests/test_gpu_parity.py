@@ -320,11 +320,13 @@ def test_fused_chain_grads_bitwise_deterministic(dev, nvox):
     x = torch.rand((1, 270, nvox, 1, 1), generator=gen, device=dev).requires_grad_(True)
     dy = torch.randn((1, 270, nvox, 1, 1), generator=gen, device=dev)
     ref = None
-    for _ in range(12):
+    for it in range(13):
         x.grad = None
         chain.zero_grad(set_to_none=True)
         chain(x).backward(dy)
         got = (x.grad.clone(), chain.lsc.sconv.weight.grad.clone(), chain.lsc.sconv.bias.grad.clone())
+        if it == 0:
+            continue   # the first call settles the fp16 pass's scale (delayed scaling); then it is fixed
         if ref is None:
             ref = got
         else:
@@ -438,10 +440,11 @@ def test_fused_chain_vs_oracle(dev, si, so, oi, oo, ni, no, grid, per_shell):
 
 
 @pytest.mark.parametrize("env", [{"DELIMIT_CHAIN_V2": "1"}, {"DELIMIT_NO_TMA": "1"},
-                                 {"DELIMIT_CHAIN_V2": "1", "DELIMIT_NO_TMA": "1"}])
+                                 {"DELIMIT_CHAIN_V2": "1", "DELIMIT_NO_TMA": "1"}, {"DELIMIT_SPLIT_TERMS": "3"}])
 def test_fallback_kernels_match_oracle(env):
-    """The fallback device paths (compact-TMEM chain kernel, cp.async input rings instead of TMA) are
-    selected per shape at run time; force them process-wide and rerun the chain parity cases."""
+    """The fallback device paths (compact-TMEM chain kernel, cp.async input rings instead of TMA, the 3-term
+    bf16 chain without the fp16 pass) are selected per shape at run time; force them process-wide and rerun
+    the chain parity cases."""
     import os
     import subprocess
     import sys
@@ -451,3 +454,41 @@ def test_fallback_kernels_match_oracle(env):
                           "-m", "gpu", "-k", "fused_chain_vs_oracle or bitwise_deterministic"],
                          env={**os.environ, **env}, capture_output=True, text=True, timeout=900, cwd=root)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ fp16 pass: delayed scaling, check, redo
+@pytest.mark.parametrize("xs,gs", [(1.0, 1.0), (1e-9, 1e-12), (3e8, 1e9), (1e-30, 1.0)])
+def test_fused_chain_scale_history(dev, xs, gs):
+    """The default chain runs an fp16 two-term pass scaled by 2^e from the previous call's magnitudes, then a
+    3-term bf16 pass that recomputes everything only if the recorded ranges were out of bounds.  Any input
+    scale gives oracle-accurate results on the first call (redo) and on later calls (rescaled fp16 pass)."""
+    rng = np.random.default_rng(11)
+    d = unit_sphere_directions(90)
+    w = rng.normal(size=(3, 3, 6)) / 18
+    b = rng.normal(size=3) * 0.1 * xs
+    s2sh = dl.Signal2SH(8, d, lb_lambda=0.006).to(dev)
+    lsc = make_lsc(d, 3, 3, 8, 8, [5], np.pi / 5, 0.006, w, b, dev)
+    chain = dl.SphericalChain(s2sh, lsc, dl.SH2Signal(8, d).to(dev))
+    grid = (13, 11, 7)
+    x = np.asarray(rng.uniform(0.1, 1.3, size=(1, 270, *grid)) * xs, np.float32).astype(np.float64)
+    dy = np.asarray(rng.normal(size=(1, 270, *grid)) * gs, np.float32).astype(np.float64)
+    M, _, _ = port.fit_operator(d, 8, 0.006)
+    geo = port.lsc_geometry(d, [5], np.pi / 5, 8, 8, 0.006)
+    Bt = port.eval_basis(d, 8)
+    wq, bq = N(lsc.sconv.weight)[:, :, 0, :], N(lsc.sconv.bias)
+    y_ref = port.chain_forward(x, M, geo, wq, bq, Bt, 3)
+    dx_ref, dW_ref, db_ref = port.chain_backward(x, dy, M, geo, wq, Bt, 3)
+    for call in range(3):
+        xt = T(x, dev, grad=True)
+        lsc.zero_grad(set_to_none=True)
+        y = chain(xt)
+        y.backward(T(dy, dev))
+        assert rel(y, y_ref) <= TOL_SH, call
+        assert rel(xt.grad, dx_ref) <= TOL_SH, call
+        assert rel(lsc.sconv.weight.grad[:, :, 0, :], dW_ref) <= TOL_LSC, call
+        assert rel(lsc.sconv.bias.grad, db_ref) <= TOL_LSC, call
+    if dl.ops.fp16_pass_enabled():
+        sf, sb = (t.cpu().numpy() for t in chain.range_state(dev))
+        assert sf[5] == 3 and sb[5] == 3                       # every call checked
+        assert sf[4] <= 1 and sb[4] <= 1                       # at most the first call was redone
+        assert sf[4] == (0 if xs == 1.0 else 1) and sb[4] == (0 if gs == 1.0 else 1)
