@@ -522,11 +522,11 @@ __device__ __forceinline__ void amax_publish(uint32_t* word, float am) {
   if ((threadIdx.x & 31) == 0) atomicMax(word, __float_as_uint(am));
 }
 
-// role r (0 IN, 1 MID, 2 MMA, 3 loader), tile it < 8, event ev < 32
+// role r < 8 (chain3v: see scripts/prof_chain_phases.py), tile it < 8, event ev < 32
 #define DL_PROF(r, ev)                                                                   \
   do {                                                                                   \
     if (p.prof && blockIdx.x == 0 && it < 8 && (threadIdx.x & 31) == 0)                  \
-      p.prof[((it)*4 + (r)) * 32 + (ev)] = clock64();                                    \
+      p.prof[((it)*8 + (r)) * 32 + (ev)] = clock64();                                    \
   } while (0)
 
 struct Bars3 {
@@ -981,6 +981,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         for (int c = 0; c < n1c; ++c) {
           const int i = g * n1c + c;
           if ((base + (uint32_t)i) % kCVQ != (uint32_t)cw) continue;
+          if ((warp & 3) == 0) DL_PROF(cw ? 6 : 5, i);
           float v[16];
           ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
           track16<H>(v, amax);
@@ -998,7 +999,9 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
               store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, w[0], w[1], vok ? p.mid_ones - 16 * i : -1);
             }
           }
+          if ((warp & 3) == 0) DL_PROF(cw ? 6 : 5, 10 + i);
           put(w);
+          if ((warp & 3) == 0) DL_PROF(cw ? 6 : 5, 20 + i);
         }
         fence_before();
         warp_arrive(&bars.d1g_free[buf]);   // this warp is done reading D1 buffer `buf`
@@ -1014,6 +1017,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
           d2_seen = true;
         }
         const int o = (i - nk2) / nk3, j = (i - nk2) - o * nk3;
+        if ((warp & 3) == 0) DL_PROF(cw ? 3 : 0, i - nk2);
         float v[16];
         ld16f(tq + p.colD2 + (uint32_t)(o * p.N2 + 16 * j), v);
         const float* bb = sb + o * p.N2 + 16 * j;
@@ -1022,7 +1026,9 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         track16<H>(v, amax);
         uint32_t w[PARTS][8];
         split16<PARTS, H>(v, w);
+        if ((warp & 3) == 0) DL_PROF(cw ? 3 : 0, 10 + i - nk2);
         put(w);
+        if ((warp & 3) == 0) DL_PROF(cw ? 3 : 0, 20 + i - nk2);
       }
     }
     if (H) amax_publish(p.rstate + kStAmaxMid, amax);
@@ -1108,16 +1114,19 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
       for (uint32_t it = 0; it < nmine; ++it) {
         for (int g = 0; g < p.G1; ++g, ++gq) {
           const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
+          DL_PROF(4, 3 * g);
           if (gq >= nb) {   // CONV has read (and stored) the group that last used this buffer
             mbar_wait_warp(&bars.d1g_free[buf], ((gq / nb) - 1) & 1);
             fence_after();
           }
+          DL_PROF(4, 3 * g + 1);
           const uint32_t d1col = tD1 + buf * (uint32_t)p.N1;
           uint64_t bd[PARTS];
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s;
           for (int k = 0; k < nk1; k += p.cpi) {   // one IN item = cpi K-steps
             mbar_wait_warp(&bars.a_full[aslot], around & 1);
+            DL_PROF(4, 10 + (g * nk1 + k) / p.cpi);
             fence_after();
             if (elect_one()) {
               kstep_ts<PARTS>(d1col, aaddr, 8, bd, id1, k == 0);

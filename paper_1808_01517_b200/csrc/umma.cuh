@@ -143,6 +143,8 @@ DL_TMEM_LD(8, "{%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
 DL_TMEM_LD(16, "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]))
+DL_TMEM_LD(32, "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+           : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]))
 #undef DL_TMEM_LD
 
 template <int N>
@@ -328,19 +330,21 @@ __device__ __forceinline__ float f16hi_to_f32(uint32_t p) {
   return f;
 }
 
-// Split (a, b) into NP fp16 parts (same packing as split_pair).  The caller scales the operands so the
-// largest magnitude sits well inside the fp16 range (delayed scaling in chain3v_tc).
+// a rounded to fp16's 11 significant bits, computed in the fp32 bit pattern (integer add + mask: no
+// conversion round trip); exactly representable in fp16 whenever a is in fp16's normal range.
+__device__ __forceinline__ float round_f16_bits(float a) {
+  return __uint_as_float((__float_as_uint(a) + 0x1000u) & 0xFFFFE000u);
+}
+
+// Split (a, b) into two fp16 parts (same packing as split_pair): hi = a rounded to 11 bits, lo = fp16(a - hi)
+// (the subtraction is exact).  The caller scales the operands so the largest magnitude sits well inside
+// the fp16 range (delayed scaling in chain3v_tc); below 2^-14 hi is rounded again (absolute error <= 2^-25).
 template <int NP>
 __device__ __forceinline__ void split_pair_h(float a, float b, uint32_t (&part)[NP]) {
-#pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    const uint32_t p = pack_f16x2(a, b);
-    part[i] = p;
-    if (i + 1 < NP) {
-      a -= f16lo_to_f32(p);
-      b -= f16hi_to_f32(p);
-    }
-  }
+  static_assert(NP == 2, "fp16 operands use two terms");
+  const float ha = round_f16_bits(a), hb = round_f16_bits(b);
+  part[0] = pack_f16x2(ha, hb);
+  part[1] = pack_f16x2(a - ha, b - hb);
 }
 
 }  // namespace umma

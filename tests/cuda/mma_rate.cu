@@ -21,7 +21,55 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
   __syncthreads();
   fence_after();
   const uint32_t tb = tb_s;
-  if (mode >= 70) {
+  if (mode >= 80) {
+    // TMEM load throughput without MMAs: warps 1..(blockDim/32-1) load for `iters` cycles.
+    // mode 80: 32x32b.x8, 81: x16, 82: x32, 83: x16 with distinct columns per warp, 84: x32 two in flight
+    long long t0 = clock64();
+    if (warp == 0 && mode >= 85) {
+      // mode 85: TS MMAs (N, D at col 0, A at col 256) back to back; 86: SS; 87: TMEM stores (x16) by warp 0
+      const uint32_t sbb = smem_u32(smem + 32768);
+      const uint64_t bd = desc_noswz(sbb, 128, 256), ad = desc_noswz(smem_u32(smem), 128, 256);
+      const uint32_t id = idesc_bf16(128, N, 0, 0);
+      long long k = 0;
+      while (clock64() - t0 < (long long)iters) {
+        if (mode == 87) {
+          uint32_t q[16];
+          for (int i = 0; i < 16; ++i) q[i] = i;
+          tmem_st<16>(tb + 256u, q);
+          tmem_wait_st();
+        } else {
+          for (int j = 0; j < 16; ++j) {
+            if (elect_one()) {
+              if (mode == 85) mma_ts(tb, tb + 256u, bd, id, 1);
+              else mma_ss(tb, ad, bd, id, 1);
+            }
+            __syncwarp();
+          }
+          if (elect_one()) commit(&mbar);
+          __syncwarp();
+          mbar_wait(&mbar, (uint32_t)(k & 1));
+        }
+        ++k;
+      }
+      if (threadIdx.x == 0) out[0] = k;
+    } else if (warp > 0) {
+      const uint32_t ta = tb + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)dcol +
+                          (mode == 83 || mode == 84 ? (uint32_t)((warp >> 2) * 64) : 0u);
+      uint32_t r[32];
+      for (int i = 0; i < 32; ++i) r[i] = i;
+      long long n = 0;
+      while (clock64() - t0 < (long long)iters) {
+        if (mode == 80) { uint32_t q[8]; tmem_ld<8>(ta, q); tmem_wait_ld(); r[0] += q[0]; }
+        else if (mode == 81 || mode == 83 || mode >= 85) { uint32_t q[16]; tmem_ld<16>(ta, q); tmem_wait_ld(); r[0] += q[0]; }
+        else if (mode == 82) { tmem_ld<32>(ta, r); tmem_wait_ld(); }
+        else { uint32_t q[16], q2[16]; tmem_ld<16>(ta, q); tmem_ld<16>(ta + 16, q2); tmem_wait_ld(); r[0] += q[0] + q2[0]; }
+        ++n;
+      }
+      if (r[0] == 12345u) out[1] = 0;
+      if ((threadIdx.x & 31) == 0 && warp == 1) out[1] = n;
+    }
+    if (threadIdx.x == 0 && mode < 85) out[0] = iters;
+  } else if (mode >= 70) {
     // the chain kernel's stage-2 pattern: B = three 144x144 K-major images (SBO 2304) 41472 bytes apart
     // in a 128 KB region, A alternating between two TMEM slots (cols 72 / 96), D at col 264 (N = 144),
     // 9 K-steps per item, a commit per K-step.  mode 71: the B images one byte-offset 0 apart (same image)
@@ -184,11 +232,22 @@ __global__ void rate_k(int mode, int N, int iters, long long* out, int dcol, int
     const uint32_t sbb = smem_u32(smem + 32768);
     const uint64_t bd = desc_noswz(sbb, 128, 256);
     const uint32_t id = idesc_bf16(128, N, 0, 0);
+    const uint64_t adss = desc_noswz(smem_u32(smem), 128, 256);
     if (warp == 0) {
       long long t0 = clock64();
-      for (int k = 0; k < iters; ++k) {
-        if (elect_one()) mma_ts(tb + (uint32_t)dcol, tb + (uint32_t)acol, bd, id, 1);
-        __syncwarp();
+      if (dcol & 0x20000) {   // control: no MMA, just wait iters * 24 cycles
+        while (clock64() - t0 < (long long)iters * 24) {
+        }
+      } else if (dcol & 0x10000) {   // A from shared memory
+        for (int k = 0; k < iters; ++k) {
+          if (elect_one()) mma_ss(tb + (uint32_t)(dcol & 0xFFFF), adss, bd, id, 1);
+          __syncwarp();
+        }
+      } else {
+        for (int k = 0; k < iters; ++k) {
+          if (elect_one()) mma_ts(tb + (uint32_t)dcol, tb + (uint32_t)acol, bd, id, 1);
+          __syncwarp();
+        }
       }
       if (elect_one()) commit(&mbar);
       __syncwarp();
@@ -286,7 +345,7 @@ extern "C" int mma_rate(int mode, int N, int iters, long long* out_host, int dco
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(rate_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const int nthr = mode >= 60 ? 32 * (1 + (acol >> 16)) : (mode >= 30 && mode < 40 ? 512 : 256);
+  const int nthr = mode >= 80 ? 32 * (1 + acol) : mode >= 60 ? 32 * (1 + (acol >> 16)) : (mode >= 30 && mode < 40 ? 512 : 256);
   rate_k<<<1, nthr, mode >= 70 ? 200 * 1024 : 64 * 1024>>>(mode, N, iters, d, dcol, acol & 0xFFFF);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(out_host, d, 16, cudaMemcpyDeviceToHost);
