@@ -523,11 +523,19 @@ __device__ __forceinline__ void amax_publish(uint32_t* word, float am) {
 }
 
 // role r < 8 (chain3v: see scripts/prof_chain_phases.py), tile it < 8, event ev < 32
+// Phase timestamps are compiled in only with -DDL_PROFILE (scripts/prof_chain_phases.py): the checks cost
+// measurable time in the conversion roles.
+#ifdef DL_PROFILE
 #define DL_PROF(r, ev)                                                                   \
   do {                                                                                   \
     if (p.prof && blockIdx.x == 0 && it < 8 && (threadIdx.x & 31) == 0)                  \
       p.prof[((it)*8 + (r)) * 32 + (ev)] = clock64();                                    \
   } while (0)
+#else
+#define DL_PROF(r, ev) \
+  do {                 \
+  } while (0)
+#endif
 
 struct Bars3 {
   uint64_t full[kMaxStages], empty[kMaxStages];   // TMA ring
