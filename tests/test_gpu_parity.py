@@ -403,6 +403,9 @@ CHAIN_CASES = [  # s_in, s_out, order_in, order_out, n_in, n_out, grid, per_shel
     (1, 1, 8, 8, 90, 90, (33, 1, 9), False),
     (2, 3, 8, 6, 60, 30, (5, 5, 5), False),      # order_out != order_in
     (1, 1, 4, 4, 30, 30, (3, 3, 3), False),
+    (3, 3, 8, 8, 90, 90, (16, 16, 4), False),    # nvox % 4 == 0, full tiles only
+    (3, 3, 8, 8, 90, 90, (30, 10, 3), False),    # nvox % 4 == 0 + partial tile
+    (3, 3, 8, 8, 90, 90, (17, 13, 6), False),    # nvox % 4 == 2 (odd channel rows 8 bytes off alignment)
 ]
 
 
