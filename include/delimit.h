@@ -131,6 +131,24 @@ int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, f
                      int64_t s_out, int64_t K, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
                      int64_t nvox, void* stream);
 
+/*
+ * Raw-acquisition ingest: b0 normalisation fused with the change to the channel-major 5-D layout.
+ * Replaces fitting.normalize_b0 (fitting.py:253-342) applied to dwio.read_nifti output (dwio.py:312-391).
+ *   raw: device copy of the stored 4-D acquisition, element (x, y, z, v) at raw[x*sx + y*sy + z*sz + v*sv]
+ *        (element strides: a NIfTI file's own bytes have sx = 1, sy = X, sz = X*Y, sv = X*Y*Z), of NIfTI
+ *        datatype code 2 (u8), 4 (i16), 8 (i32), 16 (f32) or 64 (f64), native byte order;
+ *        value = stored * slope + inter when slope != 0 (scl_slope / scl_inter).
+ *   b0_idx: n_b0 volume indices; sel: n_sel volume indices in output channel order (shell blocks).
+ *   out: (n_sel, X, Y, Z) fp32 = value / mean_b0, or 0 where mean_b0 <= 1e-6 * max(mean_b0);
+ *   excluded (optional): (X, Y, Z) bytes, 1 where excluded.  float64 arithmetic, one rounding to fp32.
+ *   workspace: dl_normalize_b0_workspace_bytes(X, Y, Z) bytes.  Index ranges are the caller's contract.
+ */
+size_t dl_normalize_b0_workspace_bytes(int64_t X, int64_t Y, int64_t Z);
+int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, int64_t Z, int64_t sx,
+                        int64_t sy, int64_t sz, int64_t sv, double slope, double inter, const int64_t* b0_idx,
+                        int64_t n_b0, const int64_t* sel, int64_t n_sel, float* out, uint8_t* excluded,
+                        void* workspace, void* stream);
+
 /* Number of kernel launches the last call on this host thread enqueued. */
 int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */

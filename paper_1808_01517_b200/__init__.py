@@ -6,7 +6,20 @@ include/delimit.h), plus a fused SphericalChain and a drop-in functional API
 mirroring the reference implementation (sphdwi 0.1.0).
 """
 
-from .errors import DelimitError, DeviceError, IllPosedFitError, KernelMismatchError, ShapeError, SphdwiError
+from .errors import (
+    DelimitError,
+    DeviceError,
+    GradientParseError,
+    IllPosedFitError,
+    KernelMismatchError,
+    MissingB0Error,
+    NiftiDatatypeError,
+    NiftiError,
+    NiftiMagicError,
+    NiftiTruncatedError,
+    ShapeError,
+    SphdwiError,
+)
 from .geometry import (
     SH_C0,
     TWO_SQRT_PI,
@@ -40,6 +53,9 @@ from .functional import (
     sh_to_signal,
     signal_to_sh,
 )
+
+from . import dwio
+from .ingest import load_dwi, normalize_b0
 
 __version__ = "0.1.0"
 

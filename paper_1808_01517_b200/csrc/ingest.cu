@@ -1,0 +1,203 @@
+// Raw-acquisition ingest: b0 normalisation fused with the layout change to the 5-D channel-major contract.
+//
+// Reference (/root/reference/pkg/src/sphdwi/): fitting.normalize_b0 (fitting.py:253-342) over the 4-D
+// acquisition dwio.read_nifti returns (dwio.py:312-391: X, Y, Z, volume, scl_slope / scl_inter applied).
+//   mean_b0 = mean of the b0 volumes per voxel (float64), eps = 1e-6 * max(mean_b0),
+//   excluded = mean_b0 <= eps (-> 0), out[k] = raw[..., sel[k]] / mean_b0 (sel = the shell volumes, shell-blocked)
+// The raw volume is read in its stored layout (NIfTI keeps x fastest, volumes slowest; an in-memory
+// (X, Y, Z, V) array keeps the volume fastest) and in its stored integer / float type: the copy to the device
+// is the file's own bytes, and one pass writes the normalised fp32 (channels, X, Y, Z) volume.
+// All arithmetic is float64 and rounds once to fp32, so results equal the reference's rounded to fp32.
+//
+// Kernels (HBM-bound streams):
+//   b0_mean_k   per-voxel b0 mean in float64, per-block maxima            reads n_b0 volumes
+//   b0_eps_k    fixed-order max of the block maxima -> eps                  (one block)
+//   ingest_k    32 x 32 shared-memory tile transpose: read coalesced along the stored fastest axis, write
+//               coalesced along z of (channel, X, Y, Z); divide / zero excluded voxels   reads n_sel volumes
+//   mask_k      excluded mask (X, Y, Z) bytes
+#include <float.h>
+
+#include "common.cuh"
+
+namespace dl {
+namespace {
+
+constexpr int kMeanBlocks = 1024;
+constexpr int kT = 32;   // transpose tile
+
+template <typename T>
+__device__ __forceinline__ double load_val(const void* raw, int64_t off, double slope, double inter) {
+  const double v = (double)reinterpret_cast<const T*>(raw)[off];
+  return slope != 0.0 ? v * slope + inter : v;
+}
+
+struct Geo {
+  int64_t X, Y, Z;          // spatial extents
+  int64_t sx, sy, sz, sv;   // element strides of the stored layout
+  int64_t e0, e1;           // spatial extents in increasing-stride order (fast, middle); the slow one is implied
+  int d0, d1, d2;           // which spatial axis (0 x, 1 y, 2 z) is fast / middle / slow in the stored layout
+};
+
+__device__ __forceinline__ void axes_of(const Geo& g, int64_t t, int64_t (&c)[3]) {
+  const int64_t a = t % g.e0, r = t / g.e0;
+  c[g.d0] = a;
+  c[g.d1] = r % g.e1;
+  c[g.d2] = r / g.e1;
+}
+
+// per-voxel mean of the b0 volumes (threads walk voxels in stored order, so b0 reads coalesce when a spatial
+// axis is the fastest); writes mean[(x * Y + y) * Z + z] and per-block maxima
+template <typename T>
+__global__ void b0_mean_k(const void* __restrict__ raw, Geo g, double slope, double inter,
+                          const int64_t* __restrict__ b0, int n_b0, double* __restrict__ mean,
+                          double* __restrict__ part) {
+  __shared__ double red[32];
+  const int64_t nvox = g.X * g.Y * g.Z;
+  double m = -DBL_MAX;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nvox; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[3];
+    axes_of(g, t, c);
+    const int64_t off = c[0] * g.sx + c[1] * g.sy + c[2] * g.sz;
+    double s = 0.0;
+    for (int i = 0; i < n_b0; ++i) s += load_val<T>(raw, off + __ldg(b0 + i) * g.sv, slope, inter);
+    const double mu = s / (double)n_b0;
+    mean[(c[0] * g.Y + c[1]) * g.Z + c[2]] = mu;
+    m = fmax(m, mu);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -DBL_MAX;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+  }
+}
+
+__global__ void b0_eps_k(const double* __restrict__ part, int nparts, int64_t nvox, double* __restrict__ eps) {
+  if (threadIdx.x == 0) {
+    double m = -DBL_MAX;
+    for (int i = 0; i < nparts; ++i) m = fmax(m, part[i]);
+    *eps = nvox > 0 ? 1e-6 * m : 0.0;
+  }
+}
+
+__global__ void mask_k(const double* __restrict__ mean, const double* __restrict__ eps, int64_t nvox,
+                       uint8_t* __restrict__ excluded) {
+  const double e = *eps;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x)
+    excluded[i] = mean[i] <= e ? 1 : 0;
+}
+
+// Tile over (a, z): a = x (xfast: the stored layout has x fastest) or a = output channel k (otherwise).
+// Grid: (ceil(A / 32), ceil(Z / 32), Y * (xfast ? n_sel : X)); block 32 x 8.
+template <typename T>
+__global__ void __launch_bounds__(256) ingest_k(const void* __restrict__ raw, Geo g, double slope, double inter,
+                                                const int64_t* __restrict__ sel, int n_sel,
+                                                const double* __restrict__ mean, const double* __restrict__ eps,
+                                                float* __restrict__ out, int xfast) {
+  __shared__ double tile[kT][kT + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t a0 = (int64_t)blockIdx.x * kT, z0 = (int64_t)blockIdx.y * kT;
+  const int64_t y = blockIdx.z % g.Y, w = blockIdx.z / g.Y;   // w = k (xfast) or x (otherwise)
+  const int64_t A = xfast ? g.X : n_sel;
+  const int64_t nvox = g.X * g.Y * g.Z;
+  // load: thread tx walks a (the stored-fast axis), rows j = z
+  for (int j = ty; j < kT; j += blockDim.y) {
+    const int64_t a = a0 + tx, z = z0 + j;
+    double v = 0.0;
+    if (a < A && z < g.Z) {
+      const int64_t x = xfast ? a : w, k = xfast ? w : a;
+      v = load_val<T>(raw, x * g.sx + y * g.sy + z * g.sz + __ldg(sel + k) * g.sv, slope, inter);
+    }
+    tile[j][tx] = v;
+  }
+  __syncthreads();
+  const double e = *eps;
+  // store: thread tx walks z, rows j = a
+  for (int j = ty; j < kT; j += blockDim.y) {
+    const int64_t a = a0 + j, z = z0 + tx;
+    if (a < A && z < g.Z) {
+      const int64_t x = xfast ? a : w, k = xfast ? w : a;
+      const int64_t vox = (x * g.Y + y) * g.Z + z;
+      const double mu = mean[vox];
+      out[k * nvox + vox] = mu <= e ? 0.f : (float)(tile[tx][j] / mu);
+    }
+  }
+}
+
+template <typename T>
+int launch_all(const void* raw, const Geo& g, double slope, double inter, const int64_t* b0, int n_b0,
+               const int64_t* sel, int n_sel, float* out, uint8_t* excluded, double* mean, double* part,
+               double* eps, cudaStream_t st) {
+  const int64_t nvox = g.X * g.Y * g.Z;
+  const int nb = (int)(ceil_div<int64_t>(nvox, 256) < kMeanBlocks ? ceil_div<int64_t>(nvox, 256) : kMeanBlocks);
+  b0_mean_k<T><<<nb, 256, 0, st>>>(raw, g, slope, inter, b0, n_b0, mean, part);
+  DL_TRY(after_launch("b0_mean_k"));
+  b0_eps_k<<<1, 32, 0, st>>>(part, nb, nvox, eps);
+  DL_TRY(after_launch("b0_eps_k"));
+  if (n_sel > 0) {
+    const int xfast = g.sx == 1 ? 1 : 0;
+    const int64_t A = xfast ? g.X : n_sel, W = xfast ? n_sel : g.X;
+    const dim3 grid((unsigned)ceil_div<int64_t>(A, kT), (unsigned)ceil_div<int64_t>(g.Z, kT), (unsigned)(g.Y * W));
+    ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, xfast);
+    DL_TRY(after_launch("ingest_k"));
+  }
+  if (excluded) {
+    const int mb = (int)(ceil_div<int64_t>(nvox, 256) < 4096 ? ceil_div<int64_t>(nvox, 256) : 4096);
+    mask_k<<<mb, 256, 0, st>>>(mean, eps, nvox, excluded);
+    DL_TRY(after_launch("mask_k"));
+  }
+  return DL_OK;
+}
+
+}  // namespace
+}  // namespace dl
+
+extern "C" {
+
+size_t dl_normalize_b0_workspace_bytes(int64_t X, int64_t Y, int64_t Z) {
+  const int64_t nvox = X * Y * Z;
+  return (size_t)(nvox > 0 ? nvox : 0) * 8 + (size_t)(dl::kMeanBlocks + 2) * 8 + 256;
+}
+
+int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, int64_t Z, int64_t sx, int64_t sy,
+                        int64_t sz, int64_t sv, double slope, double inter, const int64_t* b0_idx, int64_t n_b0,
+                        const int64_t* sel, int64_t n_sel, float* out, uint8_t* excluded, void* workspace,
+                        void* stream) {
+  using namespace dl;
+  begin_call();
+  DL_TRY(device_check(nullptr));
+  DL_REQUIRE(X >= 1 && Y >= 1 && Z >= 1 && n_b0 >= 1 && n_sel >= 0 && n_b0 < (1 << 30) && n_sel < (1 << 30),
+             "normalize_b0: bad sizes (X %lld, Y %lld, Z %lld, b0 %lld, selected %lld)", (long long)X, (long long)Y,
+             (long long)Z, (long long)n_b0, (long long)n_sel);
+  DL_REQUIRE(raw && b0_idx && workspace && (n_sel == 0 || (sel && out)), "normalize_b0: null pointer");
+  DL_REQUIRE(Y * (sx == 1 ? n_sel : X) < 2147483647LL, "normalize_b0: grid too large");
+  Geo g;
+  g.X = X; g.Y = Y; g.Z = Z; g.sx = sx; g.sy = sy; g.sz = sz; g.sv = sv;
+  // spatial axes in increasing-stride order (stable: x, y, z on ties)
+  int ord[3] = {0, 1, 2};
+  const int64_t s[3] = {sx < 0 ? -sx : sx, sy < 0 ? -sy : sy, sz < 0 ? -sz : sz};
+  for (int i = 1; i < 3; ++i)
+    for (int j = i; j > 0 && s[ord[j]] < s[ord[j - 1]]; --j) {
+      const int t = ord[j]; ord[j] = ord[j - 1]; ord[j - 1] = t;
+    }
+  const int64_t ext[3] = {X, Y, Z};
+  g.d0 = ord[0]; g.d1 = ord[1]; g.d2 = ord[2];
+  g.e0 = ext[ord[0]]; g.e1 = ext[ord[1]];
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  double* mean = reinterpret_cast<double*>(ws);
+  double* part = mean + X * Y * Z;
+  double* eps = part + kMeanBlocks;
+  cudaStream_t st = as_stream(stream);
+  switch (nifti_dtype) {
+    case 2: return launch_all<uint8_t>(raw, g, slope, inter, b0_idx, (int)n_b0, sel, (int)n_sel, out, excluded, mean, part, eps, st);
+    case 4: return launch_all<int16_t>(raw, g, slope, inter, b0_idx, (int)n_b0, sel, (int)n_sel, out, excluded, mean, part, eps, st);
+    case 8: return launch_all<int32_t>(raw, g, slope, inter, b0_idx, (int)n_b0, sel, (int)n_sel, out, excluded, mean, part, eps, st);
+    case 16: return launch_all<float>(raw, g, slope, inter, b0_idx, (int)n_b0, sel, (int)n_sel, out, excluded, mean, part, eps, st);
+    case 64: return launch_all<double>(raw, g, slope, inter, b0_idx, (int)n_b0, sel, (int)n_sel, out, excluded, mean, part, eps, st);
+    default: return fail(DL_EINVAL, "normalize_b0: unsupported NIfTI datatype code %d", nifti_dtype);
+  }
+}
+
+}  // extern "C"

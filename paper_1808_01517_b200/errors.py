@@ -28,3 +28,27 @@ class KernelMismatchError(SphdwiError):
 
 class DeviceError(SphdwiError, RuntimeError):
     """No sm_100a device, missing CUDA library, or a CUDA error from the kernels."""
+
+
+class MissingB0Error(SphdwiError):
+    """The acquisition has no b=0 volume to normalise against (errors.py:20-21)."""
+
+
+class GradientParseError(SphdwiError):
+    """A bvals / bvecs table is malformed or inconsistent (errors.py:24-25)."""
+
+
+class NiftiError(SphdwiError):
+    """Base class for NIfTI-1 read/write failures (errors.py:32-33)."""
+
+
+class NiftiMagicError(NiftiError):
+    """Not a single-file NIfTI-1 (bad sizeof_hdr / magic / dimensions / vox_offset)."""
+
+
+class NiftiDatatypeError(NiftiError):
+    """Unsupported voxel datatype code."""
+
+
+class NiftiTruncatedError(NiftiError):
+    """The file ends before the header or the voxel data it promises."""

@@ -80,6 +80,7 @@ class DwiVolume:
 
     data: torch.Tensor
     shells: int = 1
+    scheme: object = None          # dwio.GradientScheme of the channels, when known (fitting.py:69)
     check_finite: bool = True
 
     def __post_init__(self) -> None:
