@@ -12,8 +12,9 @@
 // Kernels (HBM-bound streams):
 //   b0_mean_k   per-voxel b0 mean in float64, per-block maxima            reads n_b0 volumes
 //   b0_eps_k    fixed-order max of the block maxima -> eps                  (one block)
-//   ingest_k    32 x 32 shared-memory tile transpose: read coalesced along the stored fastest axis, write
-//               coalesced along z of (channel, X, Y, Z); divide / zero excluded voxels   reads n_sel volumes
+//   ingest_x_k  32 x 32 shared-memory tile transpose for x-fastest storage (NIfTI): read along x, write along z
+//               of (channel, X, Y, Z), 48 channels per block sharing the b0 means held in registers; ingest_k: the same
+//               over (channel, z) tiles for other layouts.  Divide / zero excluded voxels.  reads n_sel volumes
 //   mask_k      excluded mask (X, Y, Z) bytes
 #include <float.h>
 
@@ -61,7 +62,9 @@ __global__ void b0_mean_k(const void* __restrict__ raw, Geo g, double slope, dou
     double s = 0.0;
     for (int i = 0; i < n_b0; ++i) s += load_val<T>(raw, off + __ldg(b0 + i) * g.sv, slope, inter);
     const double mu = s / (double)n_b0;
-    mean[(c[0] * g.Y + c[1]) * g.Z + c[2]] = mu;
+    const int64_t vox = (c[0] * g.Y + c[1]) * g.Z + c[2];
+    mean[vox] = mu;
+    mean[nvox + vox] = 1.0 / mu;   // reciprocal for the corrected-product quotient in ingest_x_k
     m = fmax(m, mu);
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -75,11 +78,10 @@ __global__ void b0_mean_k(const void* __restrict__ raw, Geo g, double slope, dou
 }
 
 __global__ void b0_eps_k(const double* __restrict__ part, int nparts, int64_t nvox, double* __restrict__ eps) {
-  if (threadIdx.x == 0) {
-    double m = -DBL_MAX;
-    for (int i = 0; i < nparts; ++i) m = fmax(m, part[i]);
-    *eps = nvox > 0 ? 1e-6 * m : 0.0;
-  }
+  double m = -DBL_MAX;   // max is order-independent: any reduction order gives the same eps
+  for (int i = threadIdx.x; i < nparts; i += 32) m = fmax(m, part[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) *eps = nvox > 0 ? 1e-6 * m : 0.0;
 }
 
 __global__ void mask_k(const double* __restrict__ mean, const double* __restrict__ eps, int64_t nvox,
@@ -89,8 +91,74 @@ __global__ void mask_k(const double* __restrict__ mean, const double* __restrict
     excluded[i] = mean[i] <= e ? 1 : 0;
 }
 
-// Tile over (a, z): a = x (xfast: the stored layout has x fastest) or a = output channel k (otherwise).
-// Grid: (ceil(A / 32), ceil(Z / 32), Y * (xfast ? n_sel : X)); block 32 x 8.
+// x-fastest stored layout (a NIfTI file's bytes): tile over (x, z) for one y and kKB consecutive output
+// channels; the tile's float64 b0 means are staged in shared memory once and reused for every channel.
+// Grid: (ceil(X / 32), ceil(Z / 32), Y * ceil(n_sel / kKB)); block 32 x 8.
+constexpr int kKB = 48;
+template <typename T>
+__global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, Geo g, double slope, double inter,
+                                                  const int64_t* __restrict__ sel, int n_sel,
+                                                  const double* __restrict__ mean, const double* __restrict__ eps,
+                                                  float* __restrict__ out) {
+  __shared__ double tile[kT][kT + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int x0 = blockIdx.x * kT, z0 = blockIdx.y * kT;
+  const int64_t y = blockIdx.z % g.Y, k0 = (blockIdx.z / g.Y) * kKB;
+  const int64_t nvox = g.X * g.Y * g.Z;
+  const double e = *eps;
+  const int X = (int)g.X, Z = (int)g.Z, sz = (int)g.sz;   // the host checks X*Y*Z < 2^31
+  // this thread's output voxels (x = x0 + j, z = z0 + tx): b0 mean and reciprocal held in registers
+  double mu[kT / 8], rc[kT / 8];
+  int vo[kT / 8];
+#pragma unroll
+  for (int q = 0; q < kT / 8; ++q) {
+    const int x = x0 + ty + 8 * q, z = z0 + tx;
+    const bool in = x < X && z < Z;
+    vo[q] = in ? (int)(((int64_t)x * g.Y + y) * Z + z) : -1;
+    mu[q] = in ? mean[vo[q]] : 1.0;
+    rc[q] = in ? mean[nvox + vo[q]] : 1.0;
+  }
+  const T* base = reinterpret_cast<const T*>(raw) + y * g.sy;
+  const int64_t k1 = k0 + kKB < n_sel ? k0 + kKB : n_sel;
+  // raw values of the next channel are loaded one iteration ahead (registers), so a block keeps two
+  // channels' reads in flight while it converts and stores the current one
+  T nxt[kT / 8];
+  auto load = [&](int64_t k) {
+    const T* src = base + __ldg(sel + k) * g.sv;
+#pragma unroll
+    for (int q = 0; q < kT / 8; ++q) {   // read along x
+      const int x = x0 + tx, z = z0 + ty + 8 * q;
+      nxt[q] = (x < X && z < Z) ? src[x + z * sz] : (T)0;
+    }
+  };
+  if (k0 < k1) load(k0);
+  for (int64_t k = k0; k < k1; ++k) {
+    T cur[kT / 8];
+#pragma unroll
+    for (int q = 0; q < kT / 8; ++q) cur[q] = nxt[q];
+    if (k + 1 < k1) load(k + 1);
+    __syncthreads();   // previous channel's tile consumed
+#pragma unroll
+    for (int q = 0; q < kT / 8; ++q) {
+      double v = (double)cur[q];
+      if (slope != 0.0) v = fma(v, slope, inter);
+      tile[ty + 8 * q][tx] = v;
+    }
+    __syncthreads();
+    float* ok = out + k * nvox;
+#pragma unroll
+    for (int q = 0; q < kT / 8; ++q) {   // out, written along z: v / mu as a corrected product
+      if (vo[q] < 0) continue;
+      const double v = tile[tx][ty + 8 * q];
+      double r = v * rc[q];
+      r = fma(fma(-r, mu[q], v), rc[q], r);
+      ok[vo[q]] = mu[q] <= e ? 0.f : (float)r;
+    }
+  }
+}
+
+// Other stored layouts (e.g. an in-memory (X, Y, Z, V) array, volume fastest): tile over (k, z) for one (x, y).
+// Grid: (ceil(n_sel / 32), ceil(Z / 32), Y * X); block 32 x 8.
 template <typename T>
 __global__ void __launch_bounds__(256) ingest_k(const void* __restrict__ raw, Geo g, double slope, double inter,
                                                 const int64_t* __restrict__ sel, int n_sel,
@@ -136,11 +204,14 @@ int launch_all(const void* raw, const Geo& g, double slope, double inter, const 
   DL_TRY(after_launch("b0_mean_k"));
   b0_eps_k<<<1, 32, 0, st>>>(part, nb, nvox, eps);
   DL_TRY(after_launch("b0_eps_k"));
-  if (n_sel > 0) {
-    const int xfast = g.sx == 1 ? 1 : 0;
-    const int64_t A = xfast ? g.X : n_sel, W = xfast ? n_sel : g.X;
-    const dim3 grid((unsigned)ceil_div<int64_t>(A, kT), (unsigned)ceil_div<int64_t>(g.Z, kT), (unsigned)(g.Y * W));
-    ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, xfast);
+  if (n_sel > 0 && g.sx == 1) {
+    const dim3 grid((unsigned)ceil_div<int64_t>(g.X, kT), (unsigned)ceil_div<int64_t>(g.Z, kT),
+                    (unsigned)(g.Y * ceil_div<int64_t>(n_sel, kKB)));
+    ingest_x_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out);
+    DL_TRY(after_launch("ingest_x_k"));
+  } else if (n_sel > 0) {
+    const dim3 grid((unsigned)ceil_div<int64_t>(n_sel, kT), (unsigned)ceil_div<int64_t>(g.Z, kT), (unsigned)(g.Y * g.X));
+    ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, 0);
     DL_TRY(after_launch("ingest_k"));
   }
   if (excluded) {
@@ -158,7 +229,7 @@ extern "C" {
 
 size_t dl_normalize_b0_workspace_bytes(int64_t X, int64_t Y, int64_t Z) {
   const int64_t nvox = X * Y * Z;
-  return (size_t)(nvox > 0 ? nvox : 0) * 8 + (size_t)(dl::kMeanBlocks + 2) * 8 + 256;
+  return (size_t)(nvox > 0 ? nvox : 0) * 16 + (size_t)(dl::kMeanBlocks + 2) * 8 + 256;
 }
 
 int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, int64_t Z, int64_t sx, int64_t sy,
@@ -172,7 +243,9 @@ int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, 
              "normalize_b0: bad sizes (X %lld, Y %lld, Z %lld, b0 %lld, selected %lld)", (long long)X, (long long)Y,
              (long long)Z, (long long)n_b0, (long long)n_sel);
   DL_REQUIRE(raw && b0_idx && workspace && (n_sel == 0 || (sel && out)), "normalize_b0: null pointer");
-  DL_REQUIRE(Y * (sx == 1 ? n_sel : X) < 2147483647LL, "normalize_b0: grid too large");
+  DL_REQUIRE(Y * (sx == 1 ? (n_sel + 47) / 48 : X) < 2147483647LL && X * Y * Z < 2147483647LL &&
+                 (sx != 1 || (sz < 2147483647LL && sz * Z < 2147483647LL)),
+             "normalize_b0: volume too large for 32-bit voxel indexing");
   Geo g;
   g.X = X; g.Y = Y; g.Z = Z; g.sx = sx; g.sy = sy; g.sz = sz; g.sv = sv;
   // spatial axes in increasing-stride order (stable: x, y, z on ties)
@@ -187,7 +260,7 @@ int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, 
   g.e0 = ext[ord[0]]; g.e1 = ext[ord[1]];
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   double* mean = reinterpret_cast<double*>(ws);
-  double* part = mean + X * Y * Z;
+  double* part = mean + 2 * X * Y * Z;   // mean | reciprocal | block maxima | eps
   double* eps = part + kMeanBlocks;
   cudaStream_t st = as_stream(stream);
   switch (nifti_dtype) {

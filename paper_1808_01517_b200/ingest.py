@@ -25,6 +25,8 @@ from .functional import DwiVolume
 from .ops import _p, _stream
 
 _CODE_OF_TORCH = {torch.uint8: 2, torch.int16: 4, torch.int32: 8, torch.float32: 16, torch.float64: 64}
+_TORCH_OF = {np.uint8: torch.uint8, np.int16: torch.int16, np.int32: torch.int32, np.float32: torch.float32,
+             np.float64: torch.float64}
 
 
 def select_volumes(bvals_or_scheme, nvol: int, b0_threshold: float = dwio.B0_THRESHOLD,
@@ -93,8 +95,10 @@ def normalize_b0(raw, bvals_or_scheme, b0_threshold: float = dwio.B0_THRESHOLD,
         strides = raw.strides()
         if raw.scaled:
             slope, inter = raw.slope, raw.inter
-        host = torch.from_numpy(np.ascontiguousarray(raw.data))
-        t = host.pin_memory().to(dev, non_blocking=True) if torch.cuda.is_available() else host
+        src = np.ascontiguousarray(raw.data)
+        host = torch.empty(src.shape, dtype=_TORCH_OF[src.dtype.type], pin_memory=torch.cuda.is_available())
+        host.numpy()[...] = src                       # the file's bytes, staged once in pinned memory
+        t = host.to(dev, non_blocking=True)
     else:
         t = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.asarray(raw))
         if t.dim() != 4:
