@@ -8,6 +8,7 @@ Writes tests/golden/ingest/:
   acq.nii.gz    int16 acquisition (9 x 7 x 6 voxels, 2 b0 + 2 shells x 6 directions, interleaved), written by
                 the reference's dwio.write_nifti, then scl_slope = 0.5 / scl_inter = 10 patched into the header
   acq.bval, acq.bvec   the gradient table (reference dwio.write_bvals_bvecs)
+  kernel_ref.json  a 2 -> 3 shell, two-ring LSC kernel written by the reference's lsc.save_kernel_json
   expected.npz  reference outputs: read_nifti data (float64, slope applied), normalize_b0 on the file's data
                 (all shells; shell 2000 only) with the exclusion mask, and normalize_b0 of an in-memory float64
                 array with a zero-b0 voxel.
@@ -26,6 +27,7 @@ import numpy as np
 sys.path.insert(0, os.environ.get("SPHDWI_REF", "/root/reference/pkg/src"))
 from sphdwi import dwio  # noqa: E402
 from sphdwi.fitting import normalize_b0  # noqa: E402
+from sphdwi.lsc import LscKernel, save_kernel_json  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ingest")
 
@@ -59,6 +61,9 @@ def main():
     np.savez_compressed(os.path.join(OUT, "expected.npz"), data=data, affine=affine, vol=vol.data, mask=mask,
                         vol_b2000=vol2.data, mask_b2000=mask2, mem=mem, vol_mem=vol3.data, mask_mem=mask3,
                         sub_bvals=vol.scheme.bvals, sub_dirs=vol.scheme.directions)
+    kw = rng.normal(size=(3, 2, 1 + 5 + 7))
+    save_kernel_json(os.path.join(OUT, "kernel_ref.json"), LscKernel(weights=kw, bias=rng.normal(size=3)), [5, 7],
+                     np.pi / 8)
     print("wrote", OUT, vol.data.shape, int(mask.sum()), vol3.data.shape, int(mask3.sum()))
 
 

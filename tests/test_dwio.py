@@ -162,3 +162,64 @@ def test_gzip_matches_plain(tmp_path):
     dwio.write_nifti(str(tmp_path / "a.nii.gz"), a)
     with gzip.open(str(tmp_path / "a.nii.gz")) as fh:
         assert fh.read() == open(str(tmp_path / "a.nii"), "rb").read()
+
+
+# --------------------------------------------------------------------------- kernel interchange (lsc.py:223-277)
+def test_kernel_json_from_reference(tmp_path):
+    from paper_1808_01517_b200 import kernel_io
+
+    k, sizes, alpha = kernel_io.load_kernel_json(os.path.join(G, "kernel_ref.json"))
+    assert sizes == (5, 7) and alpha == np.pi / 8 and k.weights.shape == (3, 2, 13)
+    p = str(tmp_path / "k.json")
+    kernel_io.save_kernel_json(p, k, sizes, alpha)
+    import json
+    ref = json.load(open(os.path.join(G, "kernel_ref.json")))
+    mine = json.load(open(p))
+    assert mine == ref                          # same document, value for value
+
+
+def test_kernel_json_errors(tmp_path):
+    import json
+
+    from paper_1808_01517_b200 import kernel_io
+    from paper_1808_01517_b200.errors import KernelMismatchError
+    from paper_1808_01517_b200.geometry import LscKernel
+
+    k = LscKernel(np.zeros((1, 1, 6)), np.zeros(1))
+    with pytest.raises(KernelMismatchError):
+        kernel_io.save_kernel_json(str(tmp_path / "a.json"), k, [7], 0.3)
+    good = dict(shells_in=1, shells_out=1, kernel_sizes=[5], angular_distance=0.3, weights=[[[0.0] * 6]], bias=[0.0])
+    for name, doc in {"missing": {k_: v for k_, v in good.items() if k_ != "bias"},
+                      "shells": {**good, "shells_in": 2},
+                      "length": {**good, "kernel_sizes": [6]}}.items():
+        q = tmp_path / f"{name}.json"
+        q.write_text(json.dumps(doc))
+        with pytest.raises(KernelMismatchError):
+            kernel_io.load_kernel_json(str(q))
+    (tmp_path / "bad.json").write_text("{not json")
+    with pytest.raises(KernelMismatchError):
+        kernel_io.load_kernel_json(str(tmp_path / "bad.json"))
+
+
+def test_module_round_trip_and_state_dict(tmp_path):
+    import torch
+
+    import paper_1808_01517_b200 as dl
+    from paper_1808_01517_b200 import kernel_io
+    from paper_1808_01517_b200.directions import unit_sphere_directions
+    from paper_1808_01517_b200.errors import KernelMismatchError
+
+    d = unit_sphere_directions(30)
+    a = dl.LocalSphericalConvolution(2, 3, 4, 4, d, [5, 7], angular_distance=np.pi / 8)
+    b = dl.LocalSphericalConvolution(2, 3, 4, 4, d, [5, 7], angular_distance=np.pi / 8)
+    kernel_io.load_module(os.path.join(G, "kernel_ref.json"), a)
+    p = str(tmp_path / "m.json")
+    kernel_io.save_module(p, a)
+    kernel_io.load_module(p, b)
+    assert torch.equal(a.sconv.weight, b.sconv.weight) and torch.equal(a.sconv.bias, b.sconv.bias)
+    c = dl.LocalSphericalConvolution(2, 3, 4, 4, d, [5, 7], angular_distance=np.pi / 8)
+    c.load_state_dict(a.state_dict())
+    assert torch.equal(c.sconv.weight, a.sconv.weight)
+    wrong = dl.LocalSphericalConvolution(2, 3, 4, 4, d, [5, 7], angular_distance=np.pi / 9)
+    with pytest.raises(KernelMismatchError):
+        kernel_io.load_module(p, wrong)
