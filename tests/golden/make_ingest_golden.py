@@ -9,6 +9,8 @@ Writes tests/golden/ingest/:
                 the reference's dwio.write_nifti, then scl_slope = 0.5 / scl_inter = 10 patched into the header
   acq.bval, acq.bvec   the gradient table (reference dwio.write_bvals_bvecs)
   kernel_ref.json  a 2 -> 3 shell, two-ring LSC kernel written by the reference's lsc.save_kernel_json
+  cli_sh.nii.gz, cli_lsc.nii.gz, cli_sig.nii.gz  the reference CLI's signal2sh (order 4) / lsc (moving
+                average 5 at pi/5) / sh2signal (shell 1000 directions) outputs on acq.nii.gz
   expected.npz  reference outputs: read_nifti data (float64, slope applied), normalize_b0 on the file's data
                 (all shells; shell 2000 only) with the exclusion mask, and normalize_b0 of an in-memory float64
                 array with a zero-b0 voxel.
@@ -64,6 +66,14 @@ def main():
     kw = rng.normal(size=(3, 2, 1 + 5 + 7))
     save_kernel_json(os.path.join(OUT, "kernel_ref.json"), LscKernel(weights=kw, bias=rng.normal(size=3)), [5, 7],
                      np.pi / 8)
+    from sphdwi.cli import main as cli
+    j = lambda n: os.path.join(OUT, n)  # noqa: E731
+    g = ["--bvals", j("acq.bval"), "--bvecs", j("acq.bvec")]
+    assert cli(["signal2sh", "--dwi", j("acq.nii.gz"), *g, "--order", "4", "--out", j("cli_sh.nii.gz")]) == 0
+    assert cli(["lsc", "--sh", j("cli_sh.nii.gz"), *g, "--moving-average", "5,0.6283185307",
+                "--out", j("cli_lsc.nii.gz")]) == 0
+    assert cli(["sh2signal", "--sh", j("cli_lsc.nii.gz"), *g, "--shell", "1000", "--order", "4",
+                "--out", j("cli_sig.nii.gz")]) == 0
     print("wrote", OUT, vol.data.shape, int(mask.sum()), vol3.data.shape, int(mask3.sum()))
 
 
