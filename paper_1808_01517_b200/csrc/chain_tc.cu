@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <utility>
 
 #include "common.cuh"
@@ -1233,6 +1234,299 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
   if (warp == kW3MMA) tmem_dealloc(tbase, 512);
 }
 
+// ============================================================================ chain2h kernel
+// The fp16 pass with SH2Signal folded into the LSC operator: y_o = T_o c + bias3_o with T_o = B' L_{o,:}
+// (forward) or dx_s = T'_s g with T'_s = M_s^T (L^T)_{s,:} (adjoint), so the tile runs two MMA stages:
+//   stage 1   D1 = x M^T per input group (issuer 1, as chain3v), into two alternating D1 buffers;
+//   CONV      D1 -> A2, the whole tile's stage-2 A operand resident in TMEM (G1 x N1 columns, two fp16
+//             terms), plus the c / g term planes for the Gram; A2 of the next tile waits for a2_free;
+//   stage 2   D3[o] = A2 T_o^T, one output group at a time into two alternating D3 buffers (issuer 2): group 0
+//             streams the A2 items as CONV hands them over, later groups reuse the resident A2;
+//   OUT       D3 -> y (x 2^-e + bias3) while the MMA fills the other D3 buffer.
+// Against chain3v this drops the D2 accumulator and its conversion pass (half of CONV's TMEM loads, splits
+// and handoffs) for ~14% more MMA work; it needs the T images (G2 x N3 x K2 fp16 pairs) in shared memory.
+constexpr int kOB2h = 2;   // D3 chunks an OUT warp loads before releasing / storing them
+struct Bars2h {
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
+  uint64_t d1g_full[2], d1g_free[2];
+  uint64_t a2_full[16], a2_free;
+  uint64_t d3_full[2], d3_free[2];
+  uint32_t tmem_base;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
+  constexpr int PARTS = 2;
+  constexpr bool H = true;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  Bars2h& bars = *reinterpret_cast<Bars2h*>(smem + p.sm_bar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kSlotW = PARTS * 8;
+  int sexp = (int)*(volatile const uint32_t*)(p.rstate + kStExp);
+  sexp = sexp < -100 ? -100 : sexp > 100 ? 100 : sexp;
+  const float sc = pow2f(sexp), isc = pow2f(-sexp);
+  float amax = 0.f;
+  {  // stage weight images + the folded bias once per CTA
+    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = (uint32_t)PARTS * p.w2_img;
+    const uint4 *s1 = reinterpret_cast<const uint4*>(p.w1), *s2 = reinterpret_cast<const uint4*>(p.w2);
+    uint4 *d1 = reinterpret_cast<uint4*>(smem + p.sm_w1), *d2 = reinterpret_cast<uint4*>(smem + p.sm_w2);
+    for (uint32_t i = threadIdx.x; i < b1 / 16; i += blockDim.x) d1[i] = __ldg(s1 + i);
+    for (uint32_t i = threadIdx.x; i < b2 / 16; i += blockDim.x) d2[i] = __ldg(s2 + i);
+    float* sb = reinterpret_cast<float*>(smem + p.sm_bias);
+    for (int i = threadIdx.x; i < p.G2 * p.N3; i += blockDim.x) {
+      const int o = i / p.N3, r = i - o * p.N3;
+      sb[i] = (p.bias2 && r < p.C3) ? __ldg(p.bias2 + o * p.C3 + r) : 0.f;
+    }
+  }
+  const int nk1 = p.K1 / 16, per_tile = p.G1 * nk1;
+  const int K2 = p.G1 * p.N1, nk2 = K2 / 16;
+  if (warp == kW3MMA) tmem_alloc(&bars.tmem_base, 512);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 4);
+    }
+    for (int s = 0; s < p.NA; ++s) {
+      mbar_init(&bars.a_full[s], 4);
+      mbar_init(&bars.a_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.d1g_full[b], 1);
+      mbar_init(&bars.d1g_free[b], kCV3);
+      mbar_init(&bars.d3_full[b], 1);
+      mbar_init(&bars.d3_free[b], kOUT3);
+    }
+    for (int k = 0; k < nk2; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting item k
+    mbar_init(&bars.a2_free, 1);
+    mbar_fence_init();
+  }
+  fence_proxy_async();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = bars.tmem_base;
+  const int64_t ntiles = p.nbatch * p.tiles_per_b;
+  auto geo = [&](int r) {
+    const int g = r / nk1, k = r - g * nk1;
+    return ChunkGeo{0, g * p.C1 + 16 * k, p.C1 - 16 * k};
+  };
+
+  if (warp < kIN3) {
+    // =========================== IN (as chain3v) ===========================
+    const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
+    if (p.tma && p.cpi == 2) {
+      if constexpr (NS % 4 == 0)
+        in_role_tma2<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
+                                                  bars.a_full, bars.a_empty,
+                                                  reinterpret_cast<const float*>(smem + p.sm_ring), bars.full,
+                                                  bars.empty, warp >> 2, sc, &amax);
+    } else if (p.tma) {
+      in_role_tma<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
+                                               bars.a_full, bars.a_empty,
+                                               reinterpret_cast<const float*>(smem + p.sm_ring), bars.full, bars.empty,
+                                               warp >> 2, 2, sc, &amax);
+    } else if (warp < 4) {
+      const float* const base[2] = {p.in, p.in};
+      const int64_t bs[2] = {p.in_bs, p.in_bs};
+      in_role_cpasync<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, base, bs, tslots,
+                                                   p.NA, bars.a_full, bars.a_empty,
+                                                   reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512, 0, 1,
+                                                   sc, &amax);
+    }
+    amax_publish(p.rstate + kStAmaxIn, amax);
+  } else if (warp < kIN3 + kCV3) {
+    // =========================== CONV: D1 -> resident A2 (+ the Gram term planes) ===========================
+    const int cw = (warp - kIN3) >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int n1c = p.N1 / 16;
+    uint32_t gq = 0, it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int64_t b = t / p.tiles_per_b, vx = (t - b * p.tiles_per_b) * kTileV + 32 * (warp & 3) + lane;
+      const bool vok = vx < p.nvox;
+      uint16_t* mid = (p.mid && vx < p.mid_pitch)
+                          ? p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2) * 64 + (vx & 63)
+                          : nullptr;
+      if (it > 0) {   // the previous tile's stage-2 MMAs have read A2
+        role_wait(&bars.a2_free, (it - 1) & 1);
+      }
+      for (int g = 0; g < p.G1; ++g, ++gq) {
+        const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
+        role_wait(&bars.d1g_full[buf], (gq / nb) & 1);
+        fence_after();
+        for (int c = 0; c < n1c; ++c) {
+          const int i = g * n1c + c;
+          if ((i & 1) != cw) continue;   // two CONV warps per quadrant alternate items
+          float v[16];
+          ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
+          track16<H>(v, amax);
+          uint32_t w[PARTS][8];
+          split16<PARTS, H>(v, w);
+          if (mid) {
+            float u[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
+            uint32_t m[2][8];
+            split16<2>(u, m);
+            store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
+          }
+          store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
+          tmem_wait_st();
+          fence_before();
+          warp_arrive(&bars.a2_full[i]);
+        }
+        fence_before();
+        warp_arrive(&bars.d1g_free[buf]);
+      }
+    }
+    amax_publish(p.rstate + kStAmaxMid, amax);
+  } else if (warp < kW3MMA) {
+    // =========================== OUT: D3 -> HBM (x 2^-e + folded bias) ===========================
+    const int ow = warp - kIN3 - kCV3, qd = warp & 3, cg = ow >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
+    const int row = 32 * qd + lane;
+    const int64_t stride = p.nvox;
+    const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
+    const int nck = p.N3 / 16;
+    uint32_t n3 = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
+      const bool vok = v < p.nvox;
+      for (int o = 0; o < p.G2; ++o, ++n3) {
+        const uint32_t xb = n3 & 1;
+        idle_wait<1>(&bars.d3_full[xb], (n3 >> 1) & 1);
+        fence_after();
+        const uint32_t d3 = tq + p.colD3 + xb * (uint32_t)p.N3;
+        for (int c0 = cg; c0 < nck; c0 += kOB2h * kOUTQ) {
+          uint32_t r[kOB2h][16];
+#pragma unroll
+          for (int k = 0; k < kOB2h; ++k)
+            if (c0 + k * kOUTQ < nck) tmem_ld<16>(d3 + (uint32_t)(c0 + k * kOUTQ) * 16, r[k]);
+          tmem_wait_ld();
+          if (c0 + kOB2h * kOUTQ >= nck) {
+            fence_before();
+            warp_arrive(&bars.d3_free[xb]);
+          }
+#pragma unroll
+          for (int k = 0; k < kOB2h; ++k) {
+            const int ck = c0 + k * kOUTQ;
+            if (ck >= nck || !vok) continue;
+            float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            const int nval = p.C3 - ck * 16;
+            const float* bb = sb + o * p.N3 + ck * 16;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              if (nval >= 16 || e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
+              d += stride;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kW3MMA || warp == kW3MMA2) {
+    // =========================== MMA issuers ===========================
+    const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2);
+    const int km = p.adjoint ? 0 : 1;   // stage 1 as chain3v; the folded T images are always K-major
+    const uint32_t id1 = idesc_f16(128, p.N1, 0, 1 - km);
+    const uint32_t id2 = idesc_f16(128, p.N3, 0, 0);
+    const int c1 = km ? p.K1 : p.N1;
+    const uint64_t ks1 = wkstep(c1, km), ks2 = wkstep(K2, 1);
+    const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    if (warp == kW3MMA) {
+      uint64_t B1[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) B1[j] = wdesc(sw1 + (uint32_t)(j * p.w1_groups) * p.w1_img, c1, km, 0);
+      const uint64_t g1s = p.w1_groups > 1 ? (uint64_t)(p.w1_img >> 4) : 0;
+      const uint32_t tA = tbase + p.colA, tD1 = tbase + p.colD1;
+      uint32_t aslot = 0, around = 0, aaddr = tA, gq = 0;
+      for (uint32_t it = 0; it < nmine; ++it) {
+        for (int g = 0; g < p.G1; ++g, ++gq) {
+          const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
+          if (gq >= nb) {
+            mbar_wait_warp(&bars.d1g_free[buf], ((gq / nb) - 1) & 1);
+            fence_after();
+          }
+          const uint32_t d1col = tD1 + buf * (uint32_t)p.N1;
+          uint64_t bd[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] = B1[j] + (uint64_t)g * g1s;
+          for (int k = 0; k < nk1; k += p.cpi) {
+            mbar_wait_warp(&bars.a_full[aslot], around & 1);
+            fence_after();
+            if (elect_one()) {
+              kstep_ts<PARTS>(d1col, aaddr, 8, bd, id1, k == 0);
+              if (p.cpi == 2) {
+                uint64_t bn[PARTS];
+#pragma unroll
+                for (int j = 0; j < PARTS; ++j) bn[j] = bd[j] + ks1;
+                kstep_ts<PARTS>(d1col, aaddr + kSlotW, 8, bn, id1, false);
+              }
+              commit(&bars.a_empty[aslot]);
+              if (k + p.cpi >= nk1) commit(&bars.d1g_full[buf]);
+            }
+            __syncwarp();
+            if (++aslot == (uint32_t)p.NA) {
+              aslot = 0;
+              ++around;
+              aaddr = tA;
+            } else {
+              aaddr += (uint32_t)p.cpi * kSlotW;
+            }
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] += (uint64_t)p.cpi * ks1;
+          }
+        }
+      }
+    } else {
+      // stage 2: T_o images, part-major (term j of group o at j * w2_img, group o rows o * N3 .. of a G2*N3 x K2 image)
+      uint64_t B2[PARTS];
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) B2[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, K2, 1, 0);
+      const uint64_t o2s = wdesc(0, K2, 1, p.N3) - wdesc(0, K2, 1, 0);
+      const uint32_t tA2 = tbase + p.colA2, tD3 = tbase + p.colD3;
+      uint32_t n3 = 0;
+      for (uint32_t it = 0; it < nmine; ++it) {
+        uint64_t bg[PARTS];
+#pragma unroll
+        for (int j = 0; j < PARTS; ++j) bg[j] = B2[j];
+        for (int o = 0; o < p.G2; ++o, ++n3) {
+          const uint32_t xb = n3 & 1;
+          if (n3 >= 2) {
+            mbar_wait_warp(&bars.d3_free[xb], ((n3 >> 1) - 1) & 1);
+            fence_after();
+          }
+          const uint32_t d3 = tD3 + xb * (uint32_t)p.N3;
+          uint64_t bd[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
+          for (int k = 0; k < nk2; ++k) {
+            if (o == 0) {
+              mbar_wait_warp(&bars.a2_full[k], it & 1);
+              fence_after();
+            }
+            if (elect_one()) kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == 0);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] += ks2;
+          }
+          if (elect_one()) {
+            commit(&bars.d3_full[xb]);
+            if (o == p.G2 - 1) commit(&bars.a2_free);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bg[j] += o2s;
+        }
+      }
+    }
+  } else if (p.tma) {
+    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kW3MMA) tmem_dealloc(tbase, 512);
+}
+
 // ============================================================================ LSC weight Gram
 // G[j][i] = sum_v g_v[j] c_v[i] over this CTA's voxels.  c = M x is written by the forward chain kernel
 // and g = B'^T dy by the adjoint, both as two-term bf16 planes (hi, next term) with rows padded per shell
@@ -1423,6 +1717,38 @@ __global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, 
   }
 }
 
+// Folded stage-2 operator of chain2h (float64 accumulation, fp32 result):
+//   forward  T[(o, n), (s, r)] = sum_q B'[n, q] L[(o, q), (s, r)],   bias3[(o, n)] = sum_q B'[n, q] bvec[(o, q)]
+//   adjoint  T[(s, i), (o, q)] = sum_r M_s[r, i] L[(o, q), (s, r)]
+// L is (s_out r_out) x (s_in r_in), B' n_out x r_out, M (mg, r_in, n).
+__global__ void fold_t_k(const float* __restrict__ L, const float* __restrict__ Bt, const float* __restrict__ M,
+                         const float* __restrict__ bvec, float* __restrict__ T, float* __restrict__ bias3, int adjoint,
+                         int s_in, int s_out, int r_in, int r_out, int n, int n_out, int mg) {
+  const int rows = adjoint ? s_in * n : s_out * n_out, cols = adjoint ? s_out * r_out : s_in * r_in;
+  const int LC = s_in * r_in;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols + (adjoint ? 0 : rows);
+       e += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (e >= rows * cols) {   // folded bias (forward)
+      const int rr = e - rows * cols, o = rr / n_out, nn = rr - o * n_out;
+      if (bvec)
+        for (int q = 0; q < r_out; ++q) acc += (double)Bt[nn * r_out + q] * (double)bvec[o * r_out + q];
+      bias3[rr] = (float)acc;
+      continue;
+    }
+    const int row = e / cols, col = e - row * cols;
+    if (!adjoint) {
+      const int o = row / n_out, nn = row - o * n_out;
+      for (int q = 0; q < r_out; ++q) acc += (double)Bt[nn * r_out + q] * (double)L[(int64_t)(o * r_out + q) * LC + col];
+    } else {
+      const int sh = row / n, i = row - sh * n, o = col / r_out, q = col - o * r_out;
+      const float* Ms = M + (int64_t)(mg > 1 ? sh : 0) * r_in * n;
+      for (int r = 0; r < r_in; ++r) acc += (double)Ms[r * n + i] * (double)L[(int64_t)(o * r_out + q) * LC + sh * r_in + r];
+    }
+    T[e] = (float)acc;
+  }
+}
+
 // fixed-order float64 reduction of the per-CTA Gram partials
 __global__ void gram_reduce_k(const float* __restrict__ partials, double* __restrict__ G, int nparts, int n) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -1526,7 +1852,7 @@ Dims make_dims(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r
 }
 
 struct WsLayout {
-  size_t imgM, imgL, imgB, imgMh, imgLh, imgBh, parts, G, total;
+  size_t imgM, imgL, imgB, imgMh, imgLh, imgBh, Tf, b3, imgTh, parts, G, total;
 };
 
 WsLayout ws_layout(const Dims& d, int nparts) {
@@ -1541,6 +1867,12 @@ WsLayout ws_layout(const Dims& d, int nparts) {
   w.imgMh = o; o = al(o + 2 * d.mg * bM, 256);   // fp16 two-term images
   w.imgLh = o; o = al(o + 2 * bL, 256);
   w.imgBh = o; o = al(o + 2 * bB, 256);
+  // chain2h: folded operator (fp32, larger of the two directions), its bias, and its fp16 image
+  const size_t tf = std::max((size_t)d.s_out * d.n_out * d.s_in * d.r_in, (size_t)d.s_in * d.n * d.s_out * d.r_out);
+  const size_t ti = std::max((size_t)d.s_out * d.NPo * d.s_in * d.RPi, (size_t)d.s_in * d.NPi * d.s_out * d.RPo) * 2;
+  w.Tf = o; o = al(o + tf * 4, 256);
+  w.b3 = o; o = al(o + (size_t)d.s_out * d.n_out * 4, 256);
+  w.imgTh = o; o = al(o + 2 * ti, 256);
   w.parts = o; o = al(o + (size_t)nparts * (GR * GC + d.s_out) * 4, 256);
   w.G = o; o = al(o + GR * GC * 8, 256);
   w.total = o;
@@ -1660,6 +1992,52 @@ bool plan_chain3v(Chain3& p, int parts) {
   return false;
 }
 
+bool use_2h() {
+  static const bool v = getenv("DELIMIT_NO_CHAIN2H") == nullptr;
+  return v;
+}
+
+// chain2h plan (fp16 pass, TMA input): TMEM = IN items | D1 x 2 | A2 (G1 N1) | D3 x 2; shared memory =
+// stage-1 image | folded T images | folded bias | TMA ring (a multiple of 4 deep) | barriers.
+bool plan_chain2h(Chain3& p) {
+  constexpr int parts = 2;
+  if (!p.tma || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2) return false;
+  const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1, A2w = p.G1 * p.N1, D3w = 2 * p.N3;
+  const int spare = 512 - D1w - A2w - D3w;
+  p.cpi = 2;
+  p.NA = spare / (2 * parts * 8);
+  if (p.NA < 2) return false;
+  if (p.NA > kMaxSlots) p.NA = kMaxSlots;
+  p.NAc = 0;
+  p.colA = 0;
+  p.colD1 = (uint32_t)(p.NA * 2 * parts * 8);
+  p.colA2 = p.colD1 + (uint32_t)D1w;
+  p.colD3 = p.colA2 + (uint32_t)A2w;
+  p.w1_img = (uint32_t)(p.N1 * p.K1 * 2);
+  p.w2_img = (uint32_t)((p.G2 * p.N3) * (p.G1 * p.N1) * 2);
+  size_t o = 0;
+  p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
+  p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
+  p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N3 * 4, 128);
+  p.sm_ring = (uint32_t)o;
+  for (int ns : {8, 4}) {
+    p.ns = ns;
+    size_t q = al(p.sm_ring + (size_t)ns * kStageBytes, 16);
+    p.sm_bar = (uint32_t)q;
+    q = al(q + sizeof(Bars2h), 16);
+    p.smem_bytes = (uint32_t)q;
+    if (q <= kSmemMax) return true;
+  }
+  return false;
+}
+
+template <int NS>
+int launch_chain2h(const Chain3& p, int grid, cudaStream_t st) {
+  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+  chain2h_tc<NS><<<grid, kThreads3, p.smem_bytes, st>>>(p);
+  return after_launch("chain2h_tc");
+}
+
 bool use_v3() {
   static const bool v = getenv("DELIMIT_CHAIN_V2") == nullptr;
   return v;
@@ -1719,10 +2097,23 @@ int run_chain3v(const Chain3& p, int grid, cudaStream_t st) {
 // default precision mode): the fp16 pass, then the bf16 pass that checks it and recomputes only if needed.
 // p's images are the bf16 ones; hw1/hw2/hw3 the fp16 images.
 int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* what, uint32_t* rstate = nullptr,
-              const uint16_t* hw1 = nullptr, const uint16_t* hw2 = nullptr, const uint16_t* hw3 = nullptr) {
+              const uint16_t* hw1 = nullptr, const uint16_t* hw2 = nullptr, const uint16_t* hw3 = nullptr,
+              const uint16_t* hT = nullptr, const float* bias3 = nullptr) {
   Chain3 v = p;
   if (use_v3() && plan_chain3v(v, d.parts)) {
-    Chain3 h = p;
+    Chain3 h = p, h2 = p;
+    if (rstate && d.parts == 3 && hw1 && hT && use_2h() && plan_chain2h(h2)) {
+      h2.w1 = hw1;
+      h2.w2 = hT;
+      h2.bias2 = bias3;
+      h2.rstate = rstate;
+      h2.redo = 0;
+      DL_TRY(h2.ns == 8 ? launch_chain2h<8>(h2, grid, st) : launch_chain2h<4>(h2, grid, st));
+      v.rstate = rstate;
+      v.redo = 1;
+      v.prof = nullptr;
+      return d.parts == 3 ? run_chain3v<3>(v, grid, st) : run_chain3v<2>(v, grid, st);
+    }
     if (rstate && d.parts == 3 && hw1 && plan_chain3v(h, 2)) {
       h.w1 = hw1;
       h.w2 = hw2;
@@ -1782,6 +2173,21 @@ int pack_all(const Dims& d, const WsLayout& w, uint8_t* ws, const float* M, cons
     DL_TRY(pack(Bt, o, oh, 1, 1, d.n_out, d.NPo, 1, d.r_out, d.RPo, d.parts, st));
   }
   return DL_OK;
+}
+
+// chain2h operands: the folded operator T (and, forward, its bias) in fp32, then its fp16 two-term image
+int fold_t(const Dims& d, const WsLayout& w, uint8_t* ws, const float* M, const float* L, const float* Bt,
+           const float* bvec, bool adjoint, cudaStream_t st) {
+  float* T = reinterpret_cast<float*>(ws + w.Tf);
+  float* b3 = reinterpret_cast<float*>(ws + w.b3);
+  const int64_t n = adjoint ? (int64_t)d.s_in * d.n * d.s_out * d.r_out : (int64_t)d.s_out * d.n_out * d.s_in * d.r_in;
+  const int blocks = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  fold_t_k<<<blocks, 256, 0, st>>>(L, Bt, M, bvec, T, b3, adjoint ? 1 : 0, d.s_in, d.s_out, d.r_in, d.r_out, d.n,
+                                   d.n_out, d.mg);
+  DL_TRY(after_launch("fold_t_k"));
+  uint16_t* img = reinterpret_cast<uint16_t*>(ws + w.imgTh);
+  if (!adjoint) return pack(T, nullptr, img, 1, d.s_out, d.n_out, d.NPo, d.s_in, d.r_in, d.RPi, 0, st);
+  return pack(T, nullptr, img, 1, d.s_in, d.n, d.NPi, d.s_out, d.r_out, d.RPo, 0, st);
 }
 
 Chain3 chain3_params(const Dims& d, const WsLayout& w, const uint8_t* ws, bool adjoint) {
@@ -1964,9 +2370,13 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   p.prof = g_prof;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
+  const bool fold = h && use_2h();
+  if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, bvec, false, st));
   return run_chain(p, d, grid, st, "chain_fwd", h ? reinterpret_cast<uint32_t*>(state) : nullptr,
                    reinterpret_cast<const uint16_t*>(ws + w.imgMh), reinterpret_cast<const uint16_t*>(ws + w.imgLh),
-                   reinterpret_cast<const uint16_t*>(ws + w.imgBh));
+                   reinterpret_cast<const uint16_t*>(ws + w.imgBh),
+                   fold ? reinterpret_cast<const uint16_t*>(ws + w.imgTh) : nullptr,
+                   reinterpret_cast<const float*>(ws + w.b3));
 }
 
 int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
@@ -2000,9 +2410,12 @@ int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, f
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
     // adjoint: stage 1 uses B' (w1 = imgB), stage 3 uses M (w3 = imgM)
+    const bool fold = h && use_2h();
+    if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, nullptr, true, st));
     DL_TRY(run_chain(p, d, grid_for(ntiles, sm), st, "chain_bwd", h ? reinterpret_cast<uint32_t*>(state) : nullptr,
                      reinterpret_cast<const uint16_t*>(ws + w.imgBh), reinterpret_cast<const uint16_t*>(ws + w.imgLh),
-                     reinterpret_cast<const uint16_t*>(ws + w.imgMh)));
+                     reinterpret_cast<const uint16_t*>(ws + w.imgMh),
+                     fold ? reinterpret_cast<const uint16_t*>(ws + w.imgTh) : nullptr, nullptr));
   }
   if (wgrad) {
     GramP g = gram_params(d, w, ws);
