@@ -1980,8 +1980,9 @@ bool plan_chain3v(Chain3& p, int parts) {
   p.sm_ring = (uint32_t)o;
   // even depths: two IN warps take alternate chunks, so each stage keeps one fixed consumer pair
   // (two-chunk items: multiples of 4)
+  static const int max_ns = getenv("DELIMIT_MAX_NS") ? atoi(getenv("DELIMIT_MAX_NS")) : 12;   // tuning knob
   for (int ns : {12, 10, 8, 6, 4, 2}) {
-    if (p.cpi == 2 && ns % 4) continue;
+    if ((p.cpi == 2 && ns % 4) || (ns > max_ns && ns > 2)) continue;
     p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)p.ns * kStageBytes, 16);
     p.sm_bar = (uint32_t)q;
