@@ -356,9 +356,15 @@ def run_ours(args):
         fwd_bytes = V * (SHELLS * NDIR + SHELLS * NDIR) * 4            # x in, y out
         bwd_bytes = V * (3 * SHELLS * NDIR) * 4                        # dy in, x-or-c in, dx out
         # dominant kernel: the fused chain kernel (forward and adjoint launches take the same time; the
-        # forward phase is one chain3v launch plus ~15 us of operator packing).  Algorithmic bytes of
-        # one launch: x in + y out (SURVEY.md 8(d), 2,160 B/voxel at cfg4).
+        # forward phase is one fp16-pass launch, the ~7 us bf16 check pass and ~25 us of operator folding /
+        # packing).  Algorithmic bytes of one launch: x in + y out (SURVEY.md 8(d), 2,160 B/voxel at cfg4).
         dom = ("chain_fwd", fwd_bytes, fwd_ms)
+        if "DELIMIT_SPLIT_TERMS" in os.environ:
+            kname = "chain3v_tc bf16 (forward phase)"
+        elif "DELIMIT_NO_CHAIN2H" in os.environ:
+            kname = "chain3v_tc fp16 pass + bf16 check (forward phase)"
+        else:
+            kname = "chain2h_tc fp16 pass + bf16 check (forward phase)"
         achieved = dom[1] / (dom[2] / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": world * V / (ms / 1e3), "unit": "voxels/s", "n_gpus": world,
@@ -370,7 +376,7 @@ def run_ours(args):
                        "channels": SHELLS * NDIR, "seq_len": None, "parallelism": f"dp{world} (subject-sharded)",
                        "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2",
                        "cuda_graph": not args.no_graph},
-            "roofline": {"bound": "hbm", "kernel": "chain3v_tc (forward)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": dom[1], "launch_ms": dom[2],
