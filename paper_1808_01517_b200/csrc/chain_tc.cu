@@ -1356,7 +1356,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
         fence_after();
         for (int c = 0; c < n1c; ++c) {
           const int i = g * n1c + c;
-          if ((i & 1) != cw) continue;   // two CONV warps per quadrant alternate items
+          if (i % kCVQ != cw) continue;   // the CONV warps of a quadrant take items round-robin
           float v[16];
           ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
           track16<H>(v, amax);
