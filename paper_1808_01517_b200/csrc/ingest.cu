@@ -45,6 +45,11 @@ __device__ __forceinline__ void axes_of(const Geo& g, int64_t t, int64_t (&c)[3]
   c[g.d1] = r % g.e1;
   c[g.d2] = r / g.e1;
 }
+// inverse of axes_of: the stored-order walk index of voxel (x, y, z); the b0 means are kept in this order
+__device__ __forceinline__ int64_t walk_of(const Geo& g, int64_t x, int64_t y, int64_t z) {
+  const int64_t c[3] = {x, y, z};
+  return c[g.d0] + g.e0 * (c[g.d1] + g.e1 * c[g.d2]);
+}
 
 // per-voxel mean of the b0 volumes (threads walk voxels in stored order, so b0 reads coalesce when a spatial
 // axis is the fastest); writes mean[(x * Y + y) * Z + z] and per-block maxima
@@ -60,11 +65,18 @@ __global__ void b0_mean_k(const void* __restrict__ raw, Geo g, double slope, dou
     axes_of(g, t, c);
     const int64_t off = c[0] * g.sx + c[1] * g.sy + c[2] * g.sz;
     double s = 0.0;
-    for (int i = 0; i < n_b0; ++i) s += load_val<T>(raw, off + __ldg(b0 + i) * g.sv, slope, inter);
+    int i = 0;
+    for (; i + 8 <= n_b0; i += 8) {   // eight loads in flight, summed in index order
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = load_val<T>(raw, off + __ldg(b0 + i + j) * g.sv, slope, inter);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; i < n_b0; ++i) s += load_val<T>(raw, off + __ldg(b0 + i) * g.sv, slope, inter);
     const double mu = s / (double)n_b0;
-    const int64_t vox = (c[0] * g.Y + c[1]) * g.Z + c[2];
-    mean[vox] = mu;
-    mean[nvox + vox] = 1.0 / mu;   // reciprocal for the corrected-product quotient in ingest_x_k
+    mean[t] = mu;              // stored (walk) order: coalesced
+    mean[nvox + t] = 1.0 / mu; // reciprocal for the corrected-product quotient
     m = fmax(m, mu);
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -84,11 +96,15 @@ __global__ void b0_eps_k(const double* __restrict__ part, int nparts, int64_t nv
   if (threadIdx.x == 0) *eps = nvox > 0 ? 1e-6 * m : 0.0;
 }
 
-__global__ void mask_k(const double* __restrict__ mean, const double* __restrict__ eps, int64_t nvox,
+// exclusion mask in (X, Y, Z) order (the x-fastest path writes it from ingest_x_k instead)
+__global__ void mask_k(Geo g, const double* __restrict__ mean, const double* __restrict__ eps,
                        uint8_t* __restrict__ excluded) {
   const double e = *eps;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x)
-    excluded[i] = mean[i] <= e ? 1 : 0;
+  const int64_t nvox = g.X * g.Y * g.Z;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % g.Z, r = i / g.Z;
+    excluded[i] = mean[walk_of(g, r / g.Y, r % g.Y, z)] <= e ? 1 : 0;
+  }
 }
 
 // x-fastest stored layout (a NIfTI file's bytes): tile over (x, z) for one y and kKB consecutive output
@@ -99,14 +115,25 @@ template <typename T>
 __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, Geo g, double slope, double inter,
                                                   const int64_t* __restrict__ sel, int n_sel,
                                                   const double* __restrict__ mean, const double* __restrict__ eps,
-                                                  float* __restrict__ out) {
-  __shared__ double tile[kT][kT + 1];
+                                                  float* __restrict__ out, uint8_t* __restrict__ excluded) {
+  __shared__ T tile[2][kT][kT + 1];      // raw values in their stored type, double-buffered
+  __shared__ double mt[2][kT][kT + 1];   // b0 means / reciprocals of the tile, [z][x] as read
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int x0 = blockIdx.x * kT, z0 = blockIdx.y * kT;
   const int64_t y = blockIdx.z % g.Y, k0 = (blockIdx.z / g.Y) * kKB;
   const int64_t nvox = g.X * g.Y * g.Z;
   const double e = *eps;
   const int X = (int)g.X, Z = (int)g.Z, sz = (int)g.sz;   // the host checks X*Y*Z < 2^31
+  // means are stored x-fastest like the input: read them along x, transpose through shared memory
+#pragma unroll
+  for (int q = 0; q < kT / 8; ++q) {
+    const int x = x0 + tx, z = z0 + ty + 8 * q;
+    const bool in = x < X && z < Z;
+    const int64_t w = walk_of(g, x, y, z);
+    mt[0][ty + 8 * q][tx] = in ? mean[w] : 1.0;
+    mt[1][ty + 8 * q][tx] = in ? mean[nvox + w] : 1.0;
+  }
+  __syncthreads();
   // this thread's output voxels (x = x0 + j, z = z0 + tx): b0 mean and reciprocal held in registers
   double mu[kT / 8], rc[kT / 8];
   int vo[kT / 8];
@@ -115,41 +142,41 @@ __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, 
     const int x = x0 + ty + 8 * q, z = z0 + tx;
     const bool in = x < X && z < Z;
     vo[q] = in ? (int)(((int64_t)x * g.Y + y) * Z + z) : -1;
-    mu[q] = in ? mean[vo[q]] : 1.0;
-    rc[q] = in ? mean[nvox + vo[q]] : 1.0;
+    mu[q] = mt[0][tx][ty + 8 * q];
+    rc[q] = mt[1][tx][ty + 8 * q];
+    if (in && excluded && k0 == 0) excluded[vo[q]] = mu[q] <= e ? 1 : 0;
   }
   const T* base = reinterpret_cast<const T*>(raw) + y * g.sy;
   const int64_t k1 = k0 + kKB < n_sel ? k0 + kKB : n_sel;
-  // raw values of the next channel are loaded one iteration ahead (registers), so a block keeps two
-  // channels' reads in flight while it converts and stores the current one
-  T nxt[kT / 8];
-  auto load = [&](int64_t k) {
+  // Raw values are loaded two channels ahead (registers) and transposed through a double-buffered
+  // shared-memory tile in their stored type, so a block keeps three channels' reads in flight and meets
+  // one barrier per channel.
+  T pa[kT / 8], pb[kT / 8];
+  auto load = [&](int64_t k, T (&dst)[kT / 8]) {
     const T* src = base + __ldg(sel + k) * g.sv;
 #pragma unroll
     for (int q = 0; q < kT / 8; ++q) {   // read along x
       const int x = x0 + tx, z = z0 + ty + 8 * q;
-      nxt[q] = (x < X && z < Z) ? src[x + z * sz] : (T)0;
+      dst[q] = (x < X && z < Z) ? src[x + z * sz] : (T)0;
     }
   };
-  if (k0 < k1) load(k0);
+  if (k0 < k1) load(k0, pa);
+  if (k0 + 1 < k1) load(k0 + 1, pb);
   for (int64_t k = k0; k < k1; ++k) {
-    T cur[kT / 8];
-#pragma unroll
-    for (int q = 0; q < kT / 8; ++q) cur[q] = nxt[q];
-    if (k + 1 < k1) load(k + 1);
-    __syncthreads();   // previous channel's tile consumed
+    const int buf = (int)((k - k0) & 1);
 #pragma unroll
     for (int q = 0; q < kT / 8; ++q) {
-      double v = (double)cur[q];
-      if (slope != 0.0) v = fma(v, slope, inter);
-      tile[ty + 8 * q][tx] = v;
+      tile[buf][ty + 8 * q][tx] = pa[q];
+      pa[q] = pb[q];
     }
+    if (k + 2 < k1) load(k + 2, pb);
     __syncthreads();
     float* ok = out + k * nvox;
 #pragma unroll
     for (int q = 0; q < kT / 8; ++q) {   // out, written along z: v / mu as a corrected product
       if (vo[q] < 0) continue;
-      const double v = tile[tx][ty + 8 * q];
+      double v = (double)tile[buf][tx][ty + 8 * q];
+      if (slope != 0.0) v = fma(v, slope, inter);
       double r = v * rc[q];
       r = fma(fma(-r, mu[q], v), rc[q], r);
       ok[vo[q]] = mu[q] <= e ? 0.f : (float)r;
@@ -188,7 +215,7 @@ __global__ void __launch_bounds__(256) ingest_k(const void* __restrict__ raw, Ge
     if (a < A && z < g.Z) {
       const int64_t x = xfast ? a : w, k = xfast ? w : a;
       const int64_t vox = (x * g.Y + y) * g.Z + z;
-      const double mu = mean[vox];
+      const double mu = mean[walk_of(g, x, y, z)];
       out[k * nvox + vox] = mu <= e ? 0.f : (float)(tile[tx][j] / mu);
     }
   }
@@ -207,8 +234,9 @@ int launch_all(const void* raw, const Geo& g, double slope, double inter, const 
   if (n_sel > 0 && g.sx == 1) {
     const dim3 grid((unsigned)ceil_div<int64_t>(g.X, kT), (unsigned)ceil_div<int64_t>(g.Z, kT),
                     (unsigned)(g.Y * ceil_div<int64_t>(n_sel, kKB)));
-    ingest_x_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out);
+    ingest_x_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, excluded);
     DL_TRY(after_launch("ingest_x_k"));
+    if (excluded) return DL_OK;   // written by ingest_x_k
   } else if (n_sel > 0) {
     const dim3 grid((unsigned)ceil_div<int64_t>(n_sel, kT), (unsigned)ceil_div<int64_t>(g.Z, kT), (unsigned)(g.Y * g.X));
     ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, 0);
@@ -216,7 +244,7 @@ int launch_all(const void* raw, const Geo& g, double slope, double inter, const 
   }
   if (excluded) {
     const int mb = (int)(ceil_div<int64_t>(nvox, 256) < 4096 ? ceil_div<int64_t>(nvox, 256) : 4096);
-    mask_k<<<mb, 256, 0, st>>>(mean, eps, nvox, excluded);
+    mask_k<<<mb, 256, 0, st>>>(g, mean, eps, excluded);
     DL_TRY(after_launch("mask_k"));
   }
   return DL_OK;
