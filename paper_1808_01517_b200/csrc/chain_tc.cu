@@ -1252,10 +1252,16 @@ struct Bars2h {
   uint64_t d1g_full[2], d1g_free[2];
   uint64_t a2_full[16], a2_free;
   uint64_t d3_full[2], d3_free[2];
+  uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
+  uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
   uint32_t tmem_base;
 };
 
-template <int NS>
+// KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
+// KOUT = true: A2 items stream through a ring (NAc slots) and stage 2 is K-outer over all output shells
+//   (D3 holds every shell; OUT releases shell o as soon as it is drained, so the next tile's first K-step
+//   into shell o can start), which removes the CONV -> stage 2 -> a2_free -> CONV cycle of the tile.
+template <int NS, bool KOUT>
 __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
   constexpr int PARTS = 2;
   constexpr bool H = true;
@@ -1299,6 +1305,11 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
     }
     for (int k = 0; k < nk2; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting item k
     mbar_init(&bars.a2_free, 1);
+    for (int c = 0; c < p.NAc; ++c) {
+      mbar_init(&bars.c_full[c], 4);
+      mbar_init(&bars.c_empty[c], 1);
+    }
+    for (int o = 0; o < 4; ++o) mbar_init(&bars.d3g_free[o], kOUT3);
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -1347,7 +1358,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
       uint16_t* mid = (p.mid && vx < p.mid_pitch)
                           ? p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2) * 64 + (vx & 63)
                           : nullptr;
-      if (it > 0) {   // the previous tile's stage-2 MMAs have read A2
+      if (!KOUT && it > 0) {   // the previous tile's stage-2 MMAs have read A2
         role_wait(&bars.a2_free, (it - 1) & 1);
       }
       for (int g = 0; g < p.G1; ++g, ++gq) {
@@ -1370,10 +1381,21 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
             split16<2>(u, m);
             store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
           }
-          store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
-          tmem_wait_st();
-          fence_before();
-          warp_arrive(&bars.a2_full[i]);
+          if constexpr (KOUT) {
+            const uint32_t ci = it * (uint32_t)nk2 + (uint32_t)i, slot = ci % (uint32_t)p.NAc,
+                           round = ci / (uint32_t)p.NAc;
+            if (round > 0) role_wait(&bars.c_empty[slot], (round - 1) & 1);
+            fence_after();
+            store_parts<PARTS>(tq + p.colA2 + slot * kSlotW, 8, w);
+            tmem_wait_st();
+            fence_before();
+            warp_arrive(&bars.c_full[slot]);
+          } else {
+            store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
+            tmem_wait_st();
+            fence_before();
+            warp_arrive(&bars.a2_full[i]);
+          }
         }
         fence_before();
         warp_arrive(&bars.d1g_free[buf]);
@@ -1392,11 +1414,17 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
-      for (int o = 0; o < p.G2; ++o, ++n3) {
-        const uint32_t xb = n3 & 1;
-        idle_wait<1>(&bars.d3_full[xb], (n3 >> 1) & 1);
+      if (KOUT) {
+        idle_wait<1>(&bars.d3_full[0], (n3 / (uint32_t)p.G2) & 1);
         fence_after();
-        const uint32_t d3 = tq + p.colD3 + xb * (uint32_t)p.N3;
+      }
+      for (int o = 0; o < p.G2; ++o, ++n3) {
+        const uint32_t xb = KOUT ? 0u : (n3 & 1);
+        if (!KOUT) {
+          idle_wait<1>(&bars.d3_full[xb], (n3 >> 1) & 1);
+          fence_after();
+        }
+        const uint32_t d3 = tq + p.colD3 + (KOUT ? (uint32_t)(o * p.N3) : xb * (uint32_t)p.N3);
         for (int c0 = cg; c0 < nck; c0 += kOB2h * kOUTQ) {
           uint32_t r[kOB2h][16];
 #pragma unroll
@@ -1405,7 +1433,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
           tmem_wait_ld();
           if (c0 + kOB2h * kOUTQ >= nck) {
             fence_before();
-            warp_arrive(&bars.d3_free[xb]);
+            warp_arrive(KOUT ? &bars.d3g_free[o] : &bars.d3_free[xb]);
           }
 #pragma unroll
           for (int k = 0; k < kOB2h; ++k) {
@@ -1485,6 +1513,39 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
       const uint64_t o2s = wdesc(0, K2, 1, p.N3) - wdesc(0, K2, 1, 0);
       const uint32_t tA2 = tbase + p.colA2, tD3 = tbase + p.colD3;
       uint32_t n3 = 0;
+      if constexpr (KOUT) {
+        uint32_t ci = 0;
+        for (uint32_t it = 0; it < nmine; ++it) {
+          uint64_t bk[PARTS];
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bk[j] = B2[j];
+          for (int k = 0; k < nk2; ++k, ++ci) {
+            const uint32_t slot = ci % (uint32_t)p.NAc, round = ci / (uint32_t)p.NAc;
+            mbar_wait_warp(&bars.c_full[slot], round & 1);
+            fence_after();
+            uint64_t bd[PARTS];
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] = bk[j];
+            for (int o = 0; o < p.G2; ++o) {
+              if (k == 0 && it > 0) {   // OUT has drained shell o of the previous tile
+                mbar_wait_warp(&bars.d3g_free[o], (it - 1) & 1);
+                fence_after();
+              }
+              if (elect_one()) kstep_ts<PARTS>(tD3 + (uint32_t)(o * p.N3), tA2 + slot * kSlotW, 8, bd, id2, k == 0);
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < PARTS; ++j) bd[j] += o2s;
+            }
+            if (elect_one()) {
+              commit(&bars.c_empty[slot]);
+              if (k == nk2 - 1) commit(&bars.d3_full[0]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bk[j] += ks2;
+          }
+        }
+      } else
       for (uint32_t it = 0; it < nmine; ++it) {
         uint64_t bg[PARTS];
 #pragma unroll
@@ -2000,16 +2061,28 @@ bool use_2h() {
 
 // chain2h plan (fp16 pass, TMA input): TMEM = IN items | D1 x 2 | A2 (G1 N1) | D3 x 2; shared memory =
 // stage-1 image | folded T images | folded bias | TMA ring (a multiple of 4 deep) | barriers.
-bool plan_chain2h(Chain3& p) {
+bool plan_chain2h(Chain3& p, bool kout) {
   constexpr int parts = 2;
-  if (!p.tma || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2) return false;
-  const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1, A2w = p.G1 * p.N1, D3w = 2 * p.N3;
-  const int spare = 512 - D1w - A2w - D3w;
+  if (!p.tma || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2 || (kout && p.G2 > 4))
+    return false;
+  const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1;
+  const int D3w = kout ? p.G2 * p.N3 : 2 * p.N3;
+  int A2w = p.G1 * p.N1;
   p.cpi = 2;
-  p.NA = spare / (2 * parts * 8);
-  if (p.NA < 2) return false;
-  if (p.NA > kMaxSlots) p.NA = kMaxSlots;
-  p.NAc = 0;
+  if (kout) {   // two IN items, the rest A2 ring slots (>= 2)
+    p.NA = 2;
+    p.NAc = (512 - D1w - D3w - 2 * 2 * parts * 8) / (parts * 8);
+    if (p.NAc > kMaxSlots) p.NAc = kMaxSlots;
+    if (p.NAc < 2) return false;
+    A2w = p.NAc * parts * 8;
+  } else {
+    const int spare = 512 - D1w - A2w - D3w;
+    p.NA = spare / (2 * parts * 8);
+    if (p.NA < 2) return false;
+    if (p.NA > kMaxSlots) p.NA = kMaxSlots;
+    p.NAc = 0;
+  }
+  if (D1w + A2w + D3w + p.NA * 2 * parts * 8 > 512) return false;
   p.colA = 0;
   p.colD1 = (uint32_t)(p.NA * 2 * parts * 8);
   p.colA2 = p.colD1 + (uint32_t)D1w;
@@ -2032,11 +2105,16 @@ bool plan_chain2h(Chain3& p) {
   return false;
 }
 
-template <int NS>
+template <int NS, bool KOUT>
 int launch_chain2h(const Chain3& p, int grid, cudaStream_t st) {
-  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
-  chain2h_tc<NS><<<grid, kThreads3, p.smem_bytes, st>>>(p);
-  return after_launch("chain2h_tc");
+  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+  chain2h_tc<NS, KOUT><<<grid, kThreads3, p.smem_bytes, st>>>(p);
+  return after_launch(KOUT ? "chain2h_tc(k-outer)" : "chain2h_tc");
+}
+
+bool use_kout() {   // DELIMIT_CHAIN2H_KOUT=1 selects the K-outer variant (measurement knob)
+  static const bool v = getenv("DELIMIT_CHAIN2H_KOUT") != nullptr;
+  return v;
 }
 
 bool use_v3() {
@@ -2103,13 +2181,15 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
   Chain3 v = p;
   if (use_v3() && plan_chain3v(v, d.parts)) {
     Chain3 h = p, h2 = p;
-    if (rstate && d.parts == 3 && hw1 && hT && use_2h() && plan_chain2h(h2)) {
+    const bool kout = use_kout();
+    if (rstate && d.parts == 3 && hw1 && hT && use_2h() && plan_chain2h(h2, kout)) {
       h2.w1 = hw1;
       h2.w2 = hT;
       h2.bias2 = bias3;
       h2.rstate = rstate;
       h2.redo = 0;
-      DL_TRY(h2.ns == 8 ? launch_chain2h<8>(h2, grid, st) : launch_chain2h<4>(h2, grid, st));
+      if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
+      else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
       v.rstate = rstate;
       v.redo = 1;
       v.prof = nullptr;

@@ -444,7 +444,7 @@ def test_fused_chain_vs_oracle(dev, si, so, oi, oo, ni, no, grid, per_shell):
 
 @pytest.mark.parametrize("env", [{"DELIMIT_CHAIN_V2": "1"}, {"DELIMIT_NO_TMA": "1"},
                                  {"DELIMIT_CHAIN_V2": "1", "DELIMIT_NO_TMA": "1"}, {"DELIMIT_SPLIT_TERMS": "3"},
-                                 {"DELIMIT_NO_CHAIN2H": "1"}])
+                                 {"DELIMIT_NO_CHAIN2H": "1"}, {"DELIMIT_CHAIN2H_KOUT": "1"}])
 def test_fallback_kernels_match_oracle(env):
     """The fallback device paths (compact-TMEM chain kernel, cp.async input rings instead of TMA, the 3-term
     bf16 chain without the fp16 pass, the three-stage fp16 chain3v instead of chain2h) are selected per shape
