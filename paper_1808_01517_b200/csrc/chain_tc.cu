@@ -468,6 +468,7 @@ struct Chain3 {
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
   uint32_t colA, colD1, colA2, colD2, colA3, colD3;
   long long* prof;                    // debug: per-role phase timestamps of CTA 0 (dl_debug_chain_prof)
+  int tstream;                        // chain2h: stream each output shell's T image from L2 into two buffers
   uint32_t* rstate;                   // chain3v delayed-scaling state (kState* words) or null
   int redo;                           // chain3v bf16 pass: check the fp16 pass's ranges, recompute if needed
 };
@@ -1254,15 +1255,18 @@ struct Bars2h {
   uint64_t d3_full[2], d3_free[2];
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
   uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
+  uint64_t t_full[2], t_empty[2];                   // tstream: T image buffers
   uint32_t tmem_base;
 };
+constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream)
+constexpr int kThreads2h = (kWT + 1) * 32;
 
 // KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
 // KOUT = true: A2 items stream through a ring (NAc slots) and stage 2 is K-outer over all output shells
 //   (D3 holds every shell; OUT releases shell o as soon as it is drained, so the next tile's first K-step
 //   into shell o can start), which removes the CONV -> stage 2 -> a2_free -> CONV cycle of the tile.
 template <int NS, bool KOUT>
-__global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
+__global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
   constexpr int PARTS = 2;
   constexpr bool H = true;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1274,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
   const float sc = pow2f(sexp), isc = pow2f(-sexp);
   float amax = 0.f;
   {  // stage weight images + the folded bias once per CTA
-    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = (uint32_t)PARTS * p.w2_img;
+    const uint32_t b1 = (uint32_t)PARTS * p.w1_groups * p.w1_img, b2 = p.tstream ? 0u : (uint32_t)PARTS * p.w2_img;
     const uint4 *s1 = reinterpret_cast<const uint4*>(p.w1), *s2 = reinterpret_cast<const uint4*>(p.w2);
     uint4 *d1 = reinterpret_cast<uint4*>(smem + p.sm_w1), *d2 = reinterpret_cast<uint4*>(smem + p.sm_w2);
     for (uint32_t i = threadIdx.x; i < b1 / 16; i += blockDim.x) d1[i] = __ldg(s1 + i);
@@ -1310,6 +1314,10 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
       mbar_init(&bars.c_empty[c], 1);
     }
     for (int o = 0; o < 4; ++o) mbar_init(&bars.d3g_free[o], kOUT3);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.t_full[b], 1);
+      mbar_init(&bars.t_empty[b], 1);
+    }
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -1511,6 +1519,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
 #pragma unroll
       for (int j = 0; j < PARTS; ++j) B2[j] = wdesc(sw2 + (uint32_t)j * p.w2_img, K2, 1, 0);
       const uint64_t o2s = wdesc(0, K2, 1, p.N3) - wdesc(0, K2, 1, 0);
+      const uint32_t tg = (uint32_t)(p.N3 * K2 * 2);   // one shell's rows of one term image
       const uint32_t tA2 = tbase + p.colA2, tD3 = tbase + p.colD3;
       uint32_t n3 = 0;
       if constexpr (KOUT) {
@@ -1558,8 +1567,15 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
           }
           const uint32_t d3 = tD3 + xb * (uint32_t)p.N3;
           uint64_t bd[PARTS];
+          if (p.tstream) {   // this shell's T image in buffer n3 & 1 (rows 0.. of the buffer)
+            mbar_wait_warp(&bars.t_full[xb], (n3 >> 1) & 1);
 #pragma unroll
-          for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
+            for (int j = 0; j < PARTS; ++j)
+              bd[j] = wdesc(sw2 + xb * (uint32_t)PARTS * tg + (uint32_t)j * tg, K2, 1, 0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
+          }
           for (int k = 0; k < nk2; ++k) {
             if (o == 0) {
               mbar_wait_warp(&bars.a2_full[k], it & 1);
@@ -1572,6 +1588,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
           }
           if (elect_one()) {
             commit(&bars.d3_full[xb]);
+            if (p.tstream) commit(&bars.t_empty[xb]);
             if (o == p.G2 - 1) commit(&bars.a2_free);
           }
           __syncwarp();
@@ -1580,8 +1597,27 @@ __global__ void __launch_bounds__(kThreads3, 1) chain2h_tc(const __grid_constant
         }
       }
     }
-  } else if (p.tma) {
-    tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
+  } else if (warp == kW3LD) {
+    if (p.tma)
+      tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
+  } else if (p.tstream) {
+    // =========================== T-image loader: shell o's rows of both term images, two buffers ===========
+    const uint32_t tg = (uint32_t)(p.N3 * K2 * 2);
+    const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    uint32_t n = 0;
+    for (uint32_t it = 0; it < nmine; ++it)
+      for (int o = 0; o < p.G2; ++o, ++n) {
+        const uint32_t b = n & 1;
+        if (n >= 2) mbar_wait_warp(&bars.t_empty[b], ((n >> 1) - 1) & 1);
+        if (elect_one()) {
+          uint8_t* dst = smem + p.sm_w2 + b * 2u * tg;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(p.w2) + (size_t)o * tg;
+          mbar_arrive_tx(&bars.t_full[b], 2u * tg);
+          bulk_g2s(dst, src, tg, &bars.t_full[b]);
+          bulk_g2s(dst + tg, src + p.w2_img, tg, &bars.t_full[b]);
+        }
+        __syncwarp();
+      }
   }
   fence_before();
   __syncthreads();
@@ -2091,10 +2127,13 @@ bool plan_chain2h(Chain3& p, bool kout) {
   p.w2_img = (uint32_t)((p.G2 * p.N3) * (p.G1 * p.N1) * 2);
   size_t o = 0;
   p.sm_w1 = (uint32_t)o; o = al(o + (size_t)parts * p.w1_groups * p.w1_img, 1024);
-  p.sm_w2 = (uint32_t)o; o = al(o + (size_t)parts * p.w2_img, 1024);
+  static const bool resident = getenv("DELIMIT_T_RESIDENT") != nullptr;   // measurement knob
+  const size_t tbufs = 2 * (size_t)parts * p.N3 * (p.G1 * p.N1) * 2;      // two shells' images
+  p.tstream = (!kout && !resident && tbufs < (size_t)parts * p.w2_img) ? 1 : 0;
+  p.sm_w2 = (uint32_t)o; o = al(o + (p.tstream ? tbufs : (size_t)parts * p.w2_img), 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N3 * 4, 128);
   p.sm_ring = (uint32_t)o;
-  for (int ns : {8, 4}) {
+  for (int ns : {12, 8, 4}) {
     p.ns = ns;
     size_t q = al(p.sm_ring + (size_t)ns * kStageBytes, 16);
     p.sm_bar = (uint32_t)q;
@@ -2108,7 +2147,7 @@ bool plan_chain2h(Chain3& p, bool kout) {
 template <int NS, bool KOUT>
 int launch_chain2h(const Chain3& p, int grid, cudaStream_t st) {
   DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
-  chain2h_tc<NS, KOUT><<<grid, kThreads3, p.smem_bytes, st>>>(p);
+  chain2h_tc<NS, KOUT><<<grid, kThreads2h, p.smem_bytes, st>>>(p);
   return after_launch(KOUT ? "chain2h_tc(k-outer)" : "chain2h_tc");
 }
 
@@ -2189,6 +2228,7 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
       h2.rstate = rstate;
       h2.redo = 0;
       if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
+      else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));
       else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
       v.rstate = rstate;
       v.redo = 1;
