@@ -149,6 +149,18 @@ int dl_normalize_b0_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, 
                         int64_t n_b0, const int64_t* sel, int64_t n_sel, float* out, uint8_t* excluded,
                         void* workspace, void* stream);
 
+/*
+ * Backward of a chain whose LSC is a product of several layers (L = L_n ... L_1, folded by the caller):
+ * dx as dl_chain_bwd_f32, plus the float64 Gram G = sum_v g c^T of g = B'^T dy and c = M x (from c_mid),
+ * rows s_out x 16-padded r_out, columns s_in x 16-padded r_in (dl_chain_gram_dims); column r_in (shell 0's
+ * first padding row) holds sum_v g.  Per-layer dW / db follow from G by small products (SphericalChain).
+ */
+int dl_chain_bwd_gram_f64(const void* c_mid, const float* dy, float* dx, double* gram, void* g_mid, const float* M,
+                          int m_per_shell, const float* L, const float* Bt, void* workspace, void* state,
+                          int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out,
+                          int64_t n_out, int64_t nvox, void* stream);
+int dl_chain_gram_dims(int64_t s_in, int64_t s_out, int64_t r_in, int64_t r_out, int64_t* rows, int64_t* cols);
+
 /* Number of kernel launches the last call on this host thread enqueued. */
 int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */

@@ -2500,23 +2500,29 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
                    reinterpret_cast<const float*>(ws + w.b3));
 }
 
-int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
-                     const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
-                     const float* beta, void* workspace, void* state, int64_t nbatch, int64_t s_in, int64_t s_out,
-                     int64_t K, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
-  using namespace dl::tc;
-  dl::begin_call();
+}  // extern "C"
+
+namespace dl {
+namespace tc {
+namespace {
+// The backward of dl_chain_bwd_f32 / dl_chain_bwd_gram_f64: gram_out (optional) receives the float64 Gram
+// instead of the finalized dW / db.
+int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* db, double* gram_out, void* g_mid,
+              const float* M, int m_per_shell, const float* L, const float* Bt, const float* P, const float* beta,
+              void* workspace, void* state, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K, int64_t n,
+              int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
   DL_REQUIRE(dy && dx && M && L && Bt && workspace, "chain_bwd: null pointer");
   DL_REQUIRE(!(dW || db) || (c_mid && g_mid && P && beta), "chain_bwd: the weight gradient needs c_mid, g_mid, P, beta");
+  DL_REQUIRE(!gram_out || (c_mid && g_mid), "chain_bwd: the Gram needs c_mid and g_mid");
   Dims d = make_dims(nbatch, s_in, s_out, n, r_in, r_out, n_out, nvox, m_per_shell);
   DL_REQUIRE(chain_fits(d), "chain_bwd: channel counts exceed the fused kernel's TMEM/smem plan");
   WsLayout w = ws_layout(d, kMaxParts);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   cudaStream_t st = dl::as_stream(stream);
   const int64_t ntiles = nbatch * ((nvox + kTileV - 1) / kTileV);
-  const bool wgrad = dW || db;
+  const bool wgrad = dW || db || gram_out;
   const bool h = state && fp16_pass();
   DL_TRY(pack_all(d, w, ws, M, L, Bt, h, st));
   if (ntiles > 0) {
@@ -2551,18 +2557,51 @@ int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, f
       nparts = grid_for(gtiles, sm < kMaxParts ? sm : kMaxParts);
       DL_TRY(run_gram(g, nparts, st));
     }
-    double* G = reinterpret_cast<double*>(ws + w.G);
+    double* G = gram_out ? gram_out : reinterpret_cast<double*>(ws + w.G);
     if (nparts == 0) {
       DL_CUDA(cudaMemsetAsync(G, 0, (size_t)GR * GC * 8, st));
     } else {
       gram_reduce_k<<<(GR * GC + 255) / 256, 256, 0, st>>>(reinterpret_cast<float*>(ws + w.parts), G, nparts, GR * GC);
       DL_TRY(dl::after_launch("gram_reduce"));
     }
+    if (!gram_out) {
     gram_finalize_k<<<(unsigned)(s_out * s_in * K + s_out), 256, 0, st>>>(G, beta, (int)r_in, P, dW, db, (int)s_out,
-                                                                          (int)s_in, (int)K, (int)r_out, (int)r_in,
-                                                                          d.RPo, d.RPi);
-    DL_TRY(dl::after_launch("gram_finalize"));
+                                                                            (int)s_in, (int)K, (int)r_out, (int)r_in,
+                                                                            d.RPo, d.RPi);
+      DL_TRY(dl::after_launch("gram_finalize"));
+    }
   }
+  return DL_OK;
+}
+}  // namespace
+}  // namespace tc
+}  // namespace dl
+
+extern "C" {
+
+int dl_chain_bwd_f32(const void* c_mid, const float* dy, float* dx, float* dW, float* db, void* g_mid,
+                     const float* M, int m_per_shell, const float* L, const float* Bt, const float* P,
+                     const float* beta, void* workspace, void* state, int64_t nbatch, int64_t s_in, int64_t s_out,
+                     int64_t K, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+  dl::begin_call();
+  return dl::tc::chain_bwd(c_mid, dy, dx, dW, db, nullptr, g_mid, M, m_per_shell, L, Bt, P, beta, workspace, state,
+                           nbatch, s_in, s_out, K, n, r_in, r_out, n_out, nvox, stream);
+}
+
+int dl_chain_bwd_gram_f64(const void* c_mid, const float* dy, float* dx, double* gram, void* g_mid, const float* M,
+                          int m_per_shell, const float* L, const float* Bt, void* workspace, void* state,
+                          int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out,
+                          int64_t n_out, int64_t nvox, void* stream) {
+  dl::begin_call();
+  if (!gram) return dl::fail(DL_EINVAL, "chain_bwd_gram: null Gram output");
+  return dl::tc::chain_bwd(c_mid, dy, dx, nullptr, nullptr, gram, g_mid, M, m_per_shell, L, Bt, nullptr, nullptr,
+                           workspace, state, nbatch, s_in, s_out, 1, n, r_in, r_out, n_out, nvox, stream);
+}
+
+int dl_chain_gram_dims(int64_t s_in, int64_t s_out, int64_t r_in, int64_t r_out, int64_t* rows, int64_t* cols) {
+  if (!rows || !cols) return dl::fail(DL_EINVAL, "chain_gram_dims: null output");
+  *rows = s_out * ((r_out + 15) / 16 * 16);
+  *cols = s_in * ((r_in + 15) / 16 * 16);
   return DL_OK;
 }
 

@@ -206,15 +206,26 @@ class SphericalChain(nn.Module):
     kernels' TMEM/shared-memory plan run the three layers one after the other instead.
     """
 
-    def __init__(self, s2sh: Signal2SH, lsc: LocalSphericalConvolution, sh2s: SH2Signal):
+    def __init__(self, s2sh: Signal2SH, lsc, sh2s: SH2Signal):
         super().__init__()
-        if s2sh.sh_order != lsc.sh_order_in:
-            raise ShapeError(f"Signal2SH order {s2sh.sh_order} does not match LSC input order {lsc.sh_order_in}")
-        if sh2s.sh_order != lsc.sh_order_out:
-            raise ShapeError(f"SH2Signal order {sh2s.sh_order} does not match LSC output order {lsc.sh_order_out}")
-        if s2sh.per_shell and len(s2sh.operators) != lsc.shells_in:
-            raise ShapeError(f"Signal2SH has {len(s2sh.operators)} shell operators, LSC expects {lsc.shells_in}")
-        self.s2sh, self.lsc, self.sh2s = s2sh, lsc, sh2s
+        layers = [lsc] if isinstance(lsc, LocalSphericalConvolution) else list(lsc)
+        if not layers or not all(isinstance(m, LocalSphericalConvolution) for m in layers):
+            raise ShapeError("lsc must be a LocalSphericalConvolution or a non-empty sequence of them")
+        first, last = layers[0], layers[-1]
+        if s2sh.sh_order != first.sh_order_in:
+            raise ShapeError(f"Signal2SH order {s2sh.sh_order} does not match LSC input order {first.sh_order_in}")
+        if sh2s.sh_order != last.sh_order_out:
+            raise ShapeError(f"SH2Signal order {sh2s.sh_order} does not match LSC output order {last.sh_order_out}")
+        if s2sh.per_shell and len(s2sh.operators) != first.shells_in:
+            raise ShapeError(f"Signal2SH has {len(s2sh.operators)} shell operators, LSC expects {first.shells_in}")
+        for a, b in zip(layers, layers[1:]):
+            if (a.shells_out, a.sh_order_out) != (b.shells_in, b.sh_order_in):
+                raise ShapeError(f"LSC layers do not chain: {a.shells_out} shells of order {a.sh_order_out} into "
+                                 f"{b.shells_in} shells of order {b.sh_order_in}")
+        # one layer: `lsc` is that module (as before); several: an nn.ModuleList in order
+        self.s2sh, self.sh2s = s2sh, sh2s
+        self.lsc = layers[0] if len(layers) == 1 else nn.ModuleList(layers)
+        self._layers = layers
         self._fused = None
         self._state = {}   # device -> (forward, adjoint) delayed-scaling state of the fp16 chain pass
 
@@ -227,20 +238,37 @@ class SphericalChain(nn.Module):
 
     def fused(self) -> bool:
         if self._fused is None:
-            self._fused = ops.chain_supported(self.lsc.shells_in, self.lsc.shells_out, self.s2sh.n_gradients,
-                                              self.lsc.r_in, self.lsc.r_out, self.sh2s.n_gradients,
-                                              self.s2sh.per_shell)
+            first, last = self._layers[0], self._layers[-1]
+            self._fused = ops.chain_supported(first.shells_in, last.shells_out, self.s2sh.n_gradients,
+                                              first.r_in, last.r_out, self.sh2s.n_gradients, self.s2sh.per_shell)
         return self._fused
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         _check_5d(x, "signal")
+        first = self._layers[0]
         s = self.s2sh.n_shells(x.shape[1])
-        if s != self.lsc.shells_in:
-            raise ShapeError(f"kernel expects {self.lsc.shells_in} input shells, volume has {s}")
-        self.lsc._validate(torch.empty((1, s * self.lsc.r_in, 1, 1, 1), device="meta"))
+        if s != first.shells_in:
+            raise ShapeError(f"kernel expects {first.shells_in} input shells, volume has {s}")
+        shells = s
+        for layer in self._layers:
+            layer._validate(torch.empty((1, shells * layer.r_in, 1, 1, 1), device="meta"))
+            shells = layer.shells_out
         x = ops.as_device_f32(x, "signal")
         if not self.fused():
-            return self.sh2s(self.lsc(self.s2sh(x)))
+            u = self.s2sh(x)
+            for layer in self._layers:
+                u = layer(u)
+            return self.sh2s(u)
+        if len(self._layers) > 1:
+            sf, sb = self.range_state(x.device)
+            args = []
+            for layer in self._layers:
+                w = layer.sconv.weight
+                b = layer.sconv.bias
+                args += [w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous(),
+                         None if b is None else b.float().contiguous(), layer.fold, layer.beta]
+            return ops.ChainStackFunction.apply(x, self.s2sh.fit_matrix, self.s2sh.per_shell, self.sh2s.basis, sf,
+                                                sb, len(self._layers), *args)
         w = self.lsc.sconv.weight
         w3 = w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous()
         b = self.lsc.sconv.bias

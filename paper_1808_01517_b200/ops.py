@@ -213,6 +213,99 @@ def chain_state(device) -> torch.Tensor:
     return torch.zeros(int(_lib.load().dl_chain_state_bytes()) // 4, dtype=torch.int32, device=device)
 
 
+class ChainStackFunction(torch.autograd.Function):
+    """Fused Signal2SH -> LSC_1 -> ... -> LSC_n -> SH2Signal (n >= 2).
+
+    The LSC layers are linear, so their product L = L_n ... L_1 and folded bias d_n (d_k = L_k d_{k-1} + bvec_k)
+    run through the same fused kernels as one layer.  The backward asks the library for the float64 Gram
+    G = sum_v g c^T and s = sum_v g (dl_chain_bwd_gram_f64); with A_k = L_{k+1}^T ... L_n^T and
+    C_{k-1} = L_{k-1} ... L_1, layer k's operator gradient is A_k G C_{k-1}^T + (A_k s) d_{k-1}^T, giving
+    dW_k = <P_k, .> and db_k = beta_k . A_k s -- no extra pass over the volume per layer.
+    layers: (weight (S_out,S_in,K), bias or None, fold (K,R_out,R_in), beta (R_out,)) per layer, in order.
+    """
+
+    @staticmethod
+    def forward(ctx, x, M, per_shell, Bt, state_fwd, state_bwd, n_layers, *layers):
+        lib = _lib.load()
+        ws_ = [layers[4 * i:4 * i + 4] for i in range(n_layers)]
+        Ls, bvecs = [], []
+        for w, b, fold, beta in ws_:
+            L, _, bvec = build_lsc_operator(fold, beta, w, b, want_Lt=False)
+            Ls.append(L.double())
+            bvecs.append(bvec.double())
+        Lt, dt = Ls[0], bvecs[0]
+        for L, bv in zip(Ls[1:], bvecs[1:]):
+            Lt, dt = L @ Lt, L @ dt + bv
+        L_tot, b_tot = Lt.float().contiguous(), dt.float().contiguous()
+        w1, f1 = ws_[0][0], ws_[0][2]
+        wn, fn = ws_[-1][0], ws_[-1][2]
+        s_in, r_in, s_out, r_out = w1.shape[1], f1.shape[2], wn.shape[0], fn.shape[1]
+        n, n_out = M.shape[-1], Bt.shape[0]
+        B, V = x.shape[0], nvox_of(x)
+        want_w = any(ctx.needs_input_grad[7:])
+        y = torch.empty((B, s_out * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
+        c_mid = _workspace(lib.dl_chain_mid_bytes(B, s_in, r_in, V), x.device) if want_w else None
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
+        _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _p(c_mid), _p(M), int(per_shell), _p(L_tot), _p(b_tot), _p(Bt),
+                  _p(ws), _p(state_fwd), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
+        ctx.save_for_backward(c_mid, M, Bt, L_tot, *[t for lay in ws_ for t in (lay[0], lay[2], lay[3])])
+        ctx.Ls, ctx.bvecs = Ls, bvecs
+        ctx.dims = (s_in, s_out, n, r_in, r_out, n_out, B, V, tuple(x.shape), n_layers)
+        ctx.has_bias = [lay[1] is not None for lay in ws_]
+        ctx.per_shell, ctx.state_bwd = per_shell, state_bwd
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        c_mid, M, Bt, L_tot, *lay = ctx.saved_tensors
+        s_in, s_out, n, r_in, r_out, n_out, B, V, xshape, nl = ctx.dims
+        lib = _lib.load()
+        dy = as_device_f32(dy, "grad")
+        nones = [None] * (7 + 4 * nl)
+        if c_mid is None and not ctx.needs_input_grad[0]:
+            return tuple(nones)
+        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
+        rows, cols = ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("dl_chain_gram_dims", s_in, s_out, r_in, r_out, ctypes.byref(rows), ctypes.byref(cols))
+        if c_mid is None:   # dx only: the single-layer entry with no weight gradient
+            _lib.call("dl_chain_bwd_f32", _NULL, _p(dy), _p(dx), _NULL, _NULL, _NULL, _p(M), int(ctx.per_shell),
+                      _p(L_tot), _p(Bt), _NULL, _NULL, _p(ws), _p(ctx.state_bwd), B, s_in, s_out, 1, n, r_in, r_out,
+                      n_out, V, _stream())
+            out = list(nones)
+            out[0] = dx
+            return tuple(out)
+        G = torch.empty((rows.value, cols.value), dtype=torch.float64, device=dy.device)
+        g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device)
+        _lib.call("dl_chain_bwd_gram_f64", _p(c_mid), _p(dy), _p(dx), _p(G), _p(g_mid), _p(M), int(ctx.per_shell),
+                  _p(L_tot), _p(Bt), _p(ws), _p(ctx.state_bwd), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
+        rpo, rpi = rows.value // s_out, cols.value // s_in
+        Gr = G.view(s_out, rpo, s_in, rpi)[:, :r_out, :, :r_in].reshape(s_out * r_out, s_in * r_in)
+        sv = G.view(s_out, rpo, cols.value)[:, :r_out, r_in].reshape(-1)
+        Ls, bvecs = ctx.Ls, ctx.bvecs
+        # C_{k-1}, d_{k-1} (input side) and A_k (output side) of every layer
+        Cs, ds = [None] * nl, [None] * nl
+        C = torch.eye(s_in * r_in, dtype=torch.float64, device=dy.device)
+        d = torch.zeros(s_in * r_in, dtype=torch.float64, device=dy.device)
+        for k in range(nl):
+            Cs[k], ds[k] = C, d
+            C, d = Ls[k] @ C, Ls[k] @ d + bvecs[k]
+        out = list(nones)
+        out[0] = dx if ctx.needs_input_grad[0] else None
+        A = torch.eye(s_out * r_out, dtype=torch.float64, device=dy.device)
+        for k in reversed(range(nl)):
+            w, fold, beta = lay[3 * k], lay[3 * k + 1], lay[3 * k + 2]
+            so, si, K = w.shape
+            ro, ri = fold.shape[1], fold.shape[2]
+            gs = A @ sv
+            dL = (A @ Gr @ Cs[k].T + torch.outer(gs, ds[k])).view(so, ro, si, ri)
+            out[7 + 4 * k] = torch.einsum("krt,orst->osk", fold.double(), dL).float()
+            if ctx.has_bias[k]:
+                out[7 + 4 * k + 1] = (gs.view(so, ro) @ beta.double()).float()
+            A = Ls[k].T @ A
+        return tuple(out)
+
+
 def fp16_pass_enabled() -> bool:
     """True when the fused chain runs the fp16 two-term pass (the default precision mode)."""
     import os

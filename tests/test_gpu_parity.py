@@ -496,3 +496,50 @@ def test_fused_chain_scale_history(dev, xs, gs):
         assert sf[5] == 3 and sb[5] == 3                       # every call checked
         assert sf[4] <= 1 and sb[4] <= 1                       # at most the first call was redone
         assert sf[4] == (0 if xs == 1.0 else 1) and sb[4] == (0 if gs == 1.0 else 1)
+
+
+# ------------------------------------------------------------------ stacked LSC layers (SURVEY cfg5 network shape)
+@pytest.mark.parametrize("layers", [[(3, 3, 8, 8), (3, 3, 8, 8)], [(3, 2, 8, 6), (2, 3, 6, 8)],
+                                    [(2, 2, 8, 8), (2, 3, 8, 8), (3, 2, 8, 8)]])
+def test_fused_chain_stacked_lsc_vs_oracle(dev, layers):
+    """Signal2SH -> LSC_1 -> ... -> LSC_n -> SH2Signal with the layers folded into one operator in the fused
+    kernels; every layer's dW / db from the one Gram (ops.ChainStackFunction) against the oracle composed layer
+    by layer (lsc.py:158-199 twice or more, and the per-stage adjoints)."""
+    rng = np.random.default_rng(len(layers) * 17 + layers[0][1])
+    d = unit_sphere_directions(90)
+    si0 = layers[0][0]
+    s2sh = dl.Signal2SH(layers[0][2], d, lb_lambda=0.006).to(dev)
+    mods, geos, ws, bs = [], [], [], []
+    for k, (si, so, oi, oo) in enumerate(layers):
+        w = rng.normal(size=(so, si, 6)) / (si * 6)
+        b = rng.normal(size=so) * 0.1
+        mods.append(make_lsc(d, si, so, oi, oo, [5], np.pi / 5, 0.006, w, b, dev))
+        geos.append(port.lsc_geometry(d, [5], np.pi / 5, oi, oo, 0.006))
+    so_n, oo_n = layers[-1][1], layers[-1][3]
+    chain = dl.SphericalChain(s2sh, mods, dl.SH2Signal(oo_n, d).to(dev))
+    assert chain.fused()
+    grid = (17, 13, 6)
+    x = np.asarray(rng.uniform(0.1, 1.3, size=(1, si0 * 90, *grid)), np.float32).astype(np.float64)
+    dy = np.asarray(rng.normal(size=(1, so_n * 90, *grid)), np.float32).astype(np.float64)
+    xt = T(x, dev, grad=True)
+    y = chain(xt)
+    y.backward(T(dy, dev))
+    M, _, _ = port.fit_operator(d, layers[0][2], 0.006)
+    Bt = port.eval_basis(d, oo_n)
+    wq = [N(m.sconv.weight)[:, :, 0, :] for m in mods]
+    bq = [N(m.sconv.bias) for m in mods]
+    us = [port.signal_to_sh(x, M, si0)]
+    for k in range(len(layers)):
+        us.append(port.lsc_forward(us[-1], wq[k], bq[k], geos[k]))
+    y_ref = port.sh_to_signal(us[-1], Bt, so_n)
+    g = port.sh_to_signal_adjoint(dy, Bt, so_n)
+    grads = [None] * len(layers)
+    for k in reversed(range(len(layers))):
+        g, dW, db = port.lsc_backward(us[k], g, wq[k], geos[k])
+        grads[k] = (dW, db)
+    dx_ref = port.signal_to_sh_adjoint(g, M, si0)
+    assert rel(y, y_ref) <= TOL_LSC
+    assert rel(xt.grad, dx_ref) <= TOL_LSC
+    for m, (dW, db) in zip(mods, grads):
+        assert rel(m.sconv.weight.grad[:, :, 0, :], dW) <= TOL_LSC
+        assert rel(m.sconv.bias.grad, db) <= TOL_LSC
