@@ -110,7 +110,8 @@ int dl_lsc_wgrad_f32(const float* g, const float* c, const float* P, const float
  * (dl_chain_mid_bytes(nbatch, s_out, r_out, nvox) bytes) when dW or db is requested; then the LSC
  * parameter gradient dW (s_out, s_in, K), db (s_out) from a streaming Gram kernel over
  * (g_mid, c_mid) plus a float64 finalize.  dW / db may be NULL (then c_mid, g_mid, P, beta may be
- * NULL).  dx must not be NULL.
+ * NULL).  dx may be NULL when dW / db are requested: the adjoint kernel then skips the dx stores (a g-only
+ * pass for training steps whose input needs no gradient).
  * workspace: dl_chain_workspace_bytes() bytes.  dl_chain_supported() says whether the
  * channel counts fit the kernels' TMEM/shared-memory plan (3 shells x order 8 x 90 dirs do).
  */

@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) chain3_tc(const __grid_constant__
         for (int ck = cg; ck < p.N3 / 16; ck += 2) {
           float vv[16];
           ld16f(tq + p.colD3 + (uint32_t)ck * 16, vv);
-          if (vok) {
+          if (vok && p.out) {   // out == null: a g-only adjoint (no dx)
             float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             const int nval = p.C3 - ck * 16;
             if (nval >= 16) {
@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #pragma unroll
             for (int e = 0; e < 16; ++e) vv[e] *= isc;
           }
-          if (vok) {
+          if (vok && p.out) {   // out == null: a g-only adjoint (no dx)
             float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             const int nval = p.C3 - ck * 16;
             if (nval >= 16) {
@@ -1446,7 +1446,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
 #pragma unroll
           for (int k = 0; k < kOB2h; ++k) {
             const int ck = c0 + k * kOUTQ;
-            if (ck >= nck || !vok) continue;
+            if (ck >= nck || !vok || !p.out) continue;
             float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             const int nval = p.C3 - ck * 16;
             const float* bb = sb + o * p.N3 + ck * 16;
@@ -2513,7 +2513,8 @@ int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* d
               int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
-  DL_REQUIRE(dy && dx && M && L && Bt && workspace, "chain_bwd: null pointer");
+  DL_REQUIRE(dy && M && L && Bt && workspace, "chain_bwd: null pointer");
+  DL_REQUIRE(dx || dW || db || gram_out, "chain_bwd: nothing requested (dx, dW, db and the Gram are all null)");
   DL_REQUIRE(!(dW || db) || (c_mid && g_mid && P && beta), "chain_bwd: the weight gradient needs c_mid, g_mid, P, beta");
   DL_REQUIRE(!gram_out || (c_mid && g_mid), "chain_bwd: the Gram needs c_mid and g_mid");
   Dims d = make_dims(nbatch, s_in, s_out, n, r_in, r_out, n_out, nvox, m_per_shell);

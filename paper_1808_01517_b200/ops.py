@@ -194,8 +194,9 @@ class ChainFunction(torch.autograd.Function):
         if not (want_x or want_w or want_b):
             return (None,) * 10
         lib = _lib.load()
-        # the adjoint kernel always runs (it produces g for the Gram); dx is discarded if not wanted
-        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
+        # the adjoint kernel always runs (it produces g for the Gram); without an input gradient it is told
+        # dx = NULL and skips the dx stores (a g-only pass)
+        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device) if want_x else None
         dW = torch.empty((s_out, s_in, K), dtype=torch.float32, device=dy.device) if want_w else None
         db = torch.empty((s_out,), dtype=torch.float32, device=dy.device) if want_b else None
         g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device) if (want_w or want_b) else None
@@ -264,7 +265,7 @@ class ChainStackFunction(torch.autograd.Function):
         nones = [None] * (7 + 4 * nl)
         if c_mid is None and not ctx.needs_input_grad[0]:
             return tuple(nones)
-        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
+        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device) if ctx.needs_input_grad[0] else None
         ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
         rows, cols = ctypes.c_int64(), ctypes.c_int64()
         _lib.call("dl_chain_gram_dims", s_in, s_out, r_in, r_out, ctypes.byref(rows), ctypes.byref(cols))

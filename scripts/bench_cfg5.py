@@ -69,8 +69,8 @@ def main(steps=20, warmup=3):
         print(json.dumps({"metric": "voxels/s, cfg5 training step (Signal2SH -> 2 x LSC -> SH2Signal, MSE, SGD)",
                           "value": world * nvox / (ms / 1e3), "unit": "voxels/s", "n_gpus": world, "steps": steps,
                           "ms_per_step": ms, "loss": float(loss), "dtype": "f32",
-                          "note": "the step includes torch's MSE loss and its gradient (two passes over y and "
-                                  "the target) and the adjoint kernel writes dx, which this step does not use"}))
+                          "note": "the step includes torch's MSE loss and its gradient (passes over y and the "
+                                  "target); x needs no gradient, so the adjoint is the g-only pass (no dx)"}))
 
 
 if __name__ == "__main__":

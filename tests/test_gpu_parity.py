@@ -543,3 +543,26 @@ def test_fused_chain_stacked_lsc_vs_oracle(dev, layers):
     for m, (dW, db) in zip(mods, grads):
         assert rel(m.sconv.weight.grad[:, :, 0, :], dW) <= TOL_LSC
         assert rel(m.sconv.bias.grad, db) <= TOL_LSC
+
+
+@pytest.mark.parametrize("stack", [1, 2])
+def test_fused_chain_weight_grads_without_dx(dev, stack):
+    """An input that needs no gradient (the usual training case) takes the g-only adjoint (dx = NULL, no dx
+    stores); the LSC gradients equal those of the full backward."""
+    rng = np.random.default_rng(31 + stack)
+    d = unit_sphere_directions(90)
+    mods = [make_lsc(d, 3, 3, 8, 8, [5], np.pi / 5, 0.006, rng.normal(size=(3, 3, 6)) / 18, rng.normal(size=3) * 0.1,
+                     dev) for _ in range(stack)]
+    chain = dl.SphericalChain(dl.Signal2SH(8, d, lb_lambda=0.006).to(dev), mods if stack > 1 else mods[0],
+                              dl.SH2Signal(8, d).to(dev))
+    x = T(rng.uniform(0.1, 1.3, size=(1, 270, 17, 13, 6)), dev)
+    dy = T(rng.normal(size=(1, 270, 17, 13, 6)), dev)
+    grads = []
+    for need_x in (True, False):
+        for m in mods:
+            m.zero_grad(set_to_none=True)
+        xi = x.clone().requires_grad_(need_x)
+        chain(xi).backward(dy)
+        grads.append([N(t) for m in mods for t in (m.sconv.weight.grad, m.sconv.bias.grad)])
+    for a, b in zip(*grads):   # the second call runs at the re-centred fp16 scale: fp32-class agreement
+        assert rel(b, a) <= 1e-5
