@@ -122,6 +122,18 @@ size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvo
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);
 size_t dl_chain_state_bytes(void);
+/*
+ * Forward fused with a mean-squared-error loss against `target` (same layout as y): writes
+ * dy = 2 (y - target) / numel(y) instead of y, and loss[2] = mean((y - target)^2) (loss: 4 doubles of
+ * device memory; [0], [1] are per-pass accumulators).  y itself is not stored.  Needs the chain3v/chain2h
+ * plan (dl_chain_mse_supported).  dy then feeds dl_chain_bwd_f32 / dl_chain_bwd_gram_f64 directly.
+ */
+int dl_chain_fwd_mse_f32(const float* x, const float* target, float* dy, void* c_mid, const float* M,
+                         int m_per_shell, const float* L, const float* bvec, const float* Bt, void* workspace,
+                         void* state, double* loss, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n,
+                         int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+int dl_chain_mse_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                           int m_per_shell);
 int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
                      const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch,
                      int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,

@@ -42,6 +42,8 @@ SIGNATURES = {
     "dl_debug_chain_prof": (None, [_c_p]),
     "dl_chain_bwd_gram_f64": (_int, [_c_p] * 6 + [_int] + [_c_p] * 4 + [_i64] * 8 + [_c_p]),
     "dl_chain_gram_dims": (_int, [_i64] * 4 + [_c_p, _c_p]),
+    "dl_chain_fwd_mse_f32": (_int, [_c_p] * 5 + [_int] + [_c_p] * 6 + [_i64] * 8 + [_c_p]),
+    "dl_chain_mse_supported": (_int, [_i64] * 6 + [_int]),
     "dl_normalize_b0_workspace_bytes": (_size, [_i64] * 3),
     "dl_normalize_b0_f32": (_int, [_c_p, _int] + [_i64] * 7 + [ctypes.c_double] * 2
                             + [_c_p, _i64, _c_p, _i64, _c_p, _c_p, _c_p, _c_p]),

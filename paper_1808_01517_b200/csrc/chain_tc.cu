@@ -469,6 +469,9 @@ struct Chain3 {
   uint32_t colA, colD1, colA2, colD2, colA3, colD3;
   long long* prof;                    // debug: per-role phase timestamps of CTA 0 (dl_debug_chain_prof)
   int tstream;                        // chain2h: stream each output shell's T image from L2 into two buffers
+  const float* target;                // fused MSE: out = out_scale * (y - target), loss[redo] += sum (y - t)^2
+  float out_scale;
+  double* loss;
   uint32_t* rstate;                   // chain3v delayed-scaling state (kState* words) or null
   int redo;                           // chain3v bf16 pass: check the fp16 pass's ranges, recompute if needed
 };
@@ -478,7 +481,7 @@ struct Chain3 {
 //   the largest scaled accumulator it converts (amax_mid); the bf16 pass launched right after checks them:
 //   in range -> every CTA exits at once; out of range -> it recomputes everything with 3-term bf16 operands
 //   (no range limits).  Its last CTA re-centres exp on the measured magnitudes and clears the words.
-enum : int { kStExp = 0, kStAmaxIn, kStAmaxMid, kStArrive, kStRedos, kStChecks, kStateWords = 8 };
+enum : int { kStExp = 0, kStAmaxIn, kStAmaxMid, kStArrive, kStRedos, kStChecks, kStLastRedo, kStateWords = 8 };
 __device__ __forceinline__ bool range_ok(float ai, float am) {
   // fp16: max 65504, 2^-24 subnormal spacing.  ai >= 2^-2 keeps the absolute rounding floor (2^-25) below
   // 2^-23 of the largest input; <= 2^14 leaves headroom for the split terms and the accumulators.
@@ -512,10 +515,18 @@ __device__ __forceinline__ bool range_check(uint32_t* st) {
     v[kStAmaxMid] = 0u;
     v[kStArrive] = 0u;
     if (!ok) v[kStRedos] = v[kStRedos] + 1u;
+    v[kStLastRedo] = ok ? 0u : 1u;   // which pass's results (and loss) stand for this call
     v[kStChecks] = v[kStChecks] + 1u;
     __threadfence();
   }
   return ok;
+}
+
+// warp sum of the squared residuals -> one float64 atomic per warp (fused MSE)
+__device__ __forceinline__ void loss_publish(double* acc, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc, v);
 }
 
 __device__ __forceinline__ void amax_publish(uint32_t* word, float am) {
@@ -1049,6 +1060,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     const int row = 32 * qd + lane;
     const int64_t stride = p.nvox;
     uint32_t n3 = 0, it = 0;
+    double lacc = 0.0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
@@ -1064,9 +1076,22 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
             for (int e = 0; e < 16; ++e) vv[e] *= isc;
           }
           if (vok && p.out) {   // out == null: a g-only adjoint (no dx)
-            float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            float* d = p.out + off;
             const int nval = p.C3 - ck * 16;
-            if (nval >= 16) {
+            if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
+              const float* tg = p.target + off;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (nval >= 16 || i < nval) {
+                  const float r = vv[i] - __ldcs(tg);
+                  lacc += (double)r * (double)r;
+                  __stcs(d, r * p.out_scale);
+                }
+                d += stride;
+                tg += stride;
+              }
+            } else if (nval >= 16) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 __stcs(d, vv[i]);
@@ -1086,6 +1111,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
         if (ow == 0) DL_PROF(1, 9 + 2 * o);
       }
     }
+    if (p.target) loss_publish(p.loss + (p.redo ? 1 : 0), lacc);
   } else if (warp == kW3MMA || warp == kW3MMA2) {
     // =========================== MMA issuers ===========================
     // Two issuing warps on different schedulers: under contention each tcgen05.mma costs the issuing
@@ -1419,6 +1445,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     const float* sb = reinterpret_cast<const float*>(smem + p.sm_bias);
     const int nck = p.N3 / 16;
     uint32_t n3 = 0;
+    double lacc = 0.0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
@@ -1447,18 +1474,34 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           for (int k = 0; k < kOB2h; ++k) {
             const int ck = c0 + k * kOUTQ;
             if (ck >= nck || !vok || !p.out) continue;
-            float* d = p.out + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+            float* d = p.out + off;
             const int nval = p.C3 - ck * 16;
             const float* bb = sb + o * p.N3 + ck * 16;
+            if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
+              const float* tg = p.target + off;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              if (nval >= 16 || e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
-              d += stride;
+              for (int e = 0; e < 16; ++e) {
+                if (nval >= 16 || e < nval) {
+                  const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - __ldcs(tg);
+                  lacc += (double)res * (double)res;
+                  __stcs(d, res * p.out_scale);
+                }
+                d += stride;
+                tg += stride;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                if (nval >= 16 || e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
+                d += stride;
+              }
             }
           }
         }
       }
     }
+    if (p.target) loss_publish(p.loss, lacc);
   } else if (warp == kW3MMA || warp == kW3MMA2) {
     // =========================== MMA issuers ===========================
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2);
@@ -2462,11 +2505,17 @@ size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvo
   return (size_t)nbatch * 2 * (size_t)(shells * r16(r)) * (size_t)mid_pitch(nvox) * 2;
 }
 
-int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
-                     const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch, int64_t s_in,
-                     int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
-  using namespace dl::tc;
-  dl::begin_call();
+}  // extern "C"
+
+namespace dl {
+namespace tc {
+namespace {
+// forward of dl_chain_fwd_f32 / dl_chain_fwd_mse_f32 (target != null: out = out_scale (y - target), squared
+// residuals summed into loss[0] by the fp16 / plain pass and into loss[1] by a redo pass)
+int chain_fwd(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
+              const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch, int64_t s_in,
+              int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream,
+              const float* target, float out_scale, double* loss) {
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
   DL_REQUIRE(x && y && M && L && Bt && workspace, "chain_fwd: null pointer");
@@ -2477,6 +2526,11 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   Chain3 p = chain3_params(d, w, ws, false);
   DL_REQUIRE(chain_fits(d), "chain_fwd: channel counts exceed the fused kernel's TMEM/smem plan");
+  if (target) {
+    Chain3 v = p;
+    DL_REQUIRE(use_v3() && plan_chain3v(v, d.parts), "chain_fwd_mse: these channel counts need the fallback kernel, "
+               "which has no fused loss (dl_chain_mse_supported)");
+  }
   if (nbatch == 0 || nvox == 0) return DL_OK;
   cudaStream_t st = dl::as_stream(stream);
   const bool h = state && fp16_pass();
@@ -2489,6 +2543,9 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   p.mid_ones = d.r_in;   // shell 0's first padding row
   p.bias2 = bvec;
   p.prof = g_prof;
+  p.target = target;
+  p.out_scale = out_scale;
+  p.loss = loss;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
   const bool fold = h && use_2h();
@@ -2498,6 +2555,50 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
                    reinterpret_cast<const uint16_t*>(ws + w.imgBh),
                    fold ? reinterpret_cast<const uint16_t*>(ws + w.imgTh) : nullptr,
                    reinterpret_cast<const float*>(ws + w.b3));
+}
+
+// the pass whose results stand decides which accumulator holds the loss
+__global__ void mse_finalize_k(const uint32_t* __restrict__ state, double* __restrict__ loss, double inv_n) {
+  const int redo = state ? (int)((volatile const uint32_t*)state)[kStLastRedo] : 0;
+  loss[2] = loss[redo ? 1 : 0] * inv_n;
+}
+}  // namespace
+}  // namespace tc
+}  // namespace dl
+
+extern "C" {
+
+int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
+                     const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch, int64_t s_in,
+                     int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+  dl::begin_call();
+  return dl::tc::chain_fwd(x, y, c_mid, M, m_per_shell, L, bvec, Bt, workspace, state, nbatch, s_in, s_out, n, r_in,
+                           r_out, n_out, nvox, stream, nullptr, 0.f, nullptr);
+}
+
+int dl_chain_fwd_mse_f32(const float* x, const float* target, float* dy, void* c_mid, const float* M, int m_per_shell,
+                         const float* L, const float* bvec, const float* Bt, void* workspace, void* state,
+                         double* loss, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
+                         int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+  dl::begin_call();
+  DL_REQUIRE(target && dy && loss, "chain_fwd_mse: null pointer");
+  const double count = (double)nbatch * (double)s_out * (double)n_out * (double)nvox;
+  cudaStream_t st = dl::as_stream(stream);
+  DL_CUDA(cudaMemsetAsync(loss, 0, 2 * sizeof(double), st));
+  DL_TRY(dl::tc::chain_fwd(x, dy, c_mid, M, m_per_shell, L, bvec, Bt, workspace, state, nbatch, s_in, s_out, n, r_in,
+                           r_out, n_out, nvox, stream, target, count > 0 ? (float)(2.0 / count) : 0.f, loss));
+  dl::tc::mse_finalize_k<<<1, 1, 0, st>>>(reinterpret_cast<const uint32_t*>(state && dl::tc::fp16_pass() ? state : nullptr),
+                                         loss, count > 0 ? 1.0 / count : 0.0);
+  return dl::after_launch("mse_finalize_k");
+}
+
+int dl_chain_mse_supported(int64_t s_in, int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out,
+                           int m_per_shell) {
+  using namespace dl::tc;
+  const Dims d = make_dims(1, s_in, s_out, n, r_in, r_out, n_out, 1, m_per_shell);
+  if (!chain_fits(d) || !use_v3()) return 0;
+  Chain3 v = chain3_params(d, ws_layout(d, 1), nullptr, false);
+  return plan_chain3v(v, d.parts) ? 1 : 0;
 }
 
 }  // extern "C"

@@ -236,6 +236,36 @@ class SphericalChain(nn.Module):
             self._state[key] = (ops.chain_state(device), ops.chain_state(device))
         return self._state[key]
 
+    def mse_loss(self, x: torch.Tensor, target: torch.Tensor, fused: bool = False) -> torch.Tensor:
+        """mean((self(x) - target)^2).
+
+        fused=True computes the loss and its gradient inside the forward kernel (ops.ChainMseFunction: dy is
+        written in place of y).  It is parity-tested but measured slower at cfg5 (17.0 vs 10.5 ms per training
+        step): the OUT warps' target loads stall the pipeline.  The default is the chain output and torch's MSE.
+        """
+        first, last = self._layers[0], self._layers[-1]
+        if not (fused and self.fused() and ops.chain_mse_supported(first.shells_in, last.shells_out,
+                                                                   self.s2sh.n_gradients, first.r_in, last.r_out,
+                                                                   self.sh2s.n_gradients, self.s2sh.per_shell)):
+            return torch.nn.functional.mse_loss(self(x), target)
+        _check_5d(x, "signal")
+        s = self.s2sh.n_shells(x.shape[1])
+        if s != first.shells_in:
+            raise ShapeError(f"kernel expects {first.shells_in} input shells, volume has {s}")
+        shells = s
+        for layer in self._layers:
+            layer._validate(torch.empty((1, shells * layer.r_in, 1, 1, 1), device="meta"))
+            shells = layer.shells_out
+        x = ops.as_device_f32(x, "signal")
+        sf, sb = self.range_state(x.device)
+        args = []
+        for layer in self._layers:
+            w, b = layer.sconv.weight, layer.sconv.bias
+            args += [w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous(),
+                     None if b is None else b.float().contiguous(), layer.fold, layer.beta]
+        return ops.ChainMseFunction.apply(x, target, self.s2sh.fit_matrix, self.s2sh.per_shell, self.sh2s.basis, sf,
+                                          sb, len(self._layers), *args)
+
     def fused(self) -> bool:
         if self._fused is None:
             first, last = self._layers[0], self._layers[-1]

@@ -307,6 +307,124 @@ class ChainStackFunction(torch.autograd.Function):
         return tuple(out)
 
 
+def _fold_layers(layers):
+    """Per-layer (L_k, bvec_k) in float64 and the product L = L_n ... L_1 with its folded bias."""
+    Ls, bvecs = [], []
+    for w, b, fold, beta in layers:
+        L, _, bvec = build_lsc_operator(fold, beta, w, b, want_Lt=False)
+        Ls.append(L.double())
+        bvecs.append(bvec.double())
+    Lt, dt = Ls[0], bvecs[0]
+    for L, bv in zip(Ls[1:], bvecs[1:]):
+        Lt, dt = L @ Lt, L @ dt + bv
+    return Ls, bvecs, Lt.float().contiguous(), dt.float().contiguous()
+
+
+def _layer_grads(G, rows, cols, dims, Ls, bvecs, lay, has_bias, device):
+    """Per-layer dW / db from the float64 Gram (see ChainStackFunction); `lay` = (w, fold, beta) per layer."""
+    s_in, s_out, r_in, r_out, nl = dims
+    rpo, rpi = rows // s_out, cols // s_in
+    Gr = G.view(s_out, rpo, s_in, rpi)[:, :r_out, :, :r_in].reshape(s_out * r_out, s_in * r_in)
+    sv = G.view(s_out, rpo, cols)[:, :r_out, r_in].reshape(-1)
+    Cs, ds = [None] * nl, [None] * nl
+    C = torch.eye(s_in * r_in, dtype=torch.float64, device=device)
+    d = torch.zeros(s_in * r_in, dtype=torch.float64, device=device)
+    for k in range(nl):
+        Cs[k], ds[k] = C, d
+        C, d = Ls[k] @ C, Ls[k] @ d + bvecs[k]
+    out = [None] * (2 * nl)
+    A = torch.eye(s_out * r_out, dtype=torch.float64, device=device)
+    for k in reversed(range(nl)):
+        w, fold, beta = lay[3 * k], lay[3 * k + 1], lay[3 * k + 2]
+        so, si, K = w.shape
+        ro, ri = fold.shape[1], fold.shape[2]
+        gs = A @ sv
+        dL = (A @ Gr @ Cs[k].T + torch.outer(gs, ds[k])).view(so, ro, si, ri)
+        out[2 * k] = torch.einsum("krt,orst->osk", fold.double(), dL).float()
+        if has_bias[k]:
+            out[2 * k + 1] = (gs.view(so, ro) @ beta.double()).float()
+        A = Ls[k].T @ A
+    return out
+
+
+class ChainMseFunction(torch.autograd.Function):
+    """mean((chain(x) - target)^2) with the loss and its gradient fused into the forward kernel.
+
+    dl_chain_fwd_mse_f32 writes dy = 2 (y - target) / numel(y) in place of y and reduces the loss; the
+    backward runs the adjoint on that dy (g-only when x needs no gradient) and takes every layer's dW / db from
+    the one float64 Gram.  One or more LSC layers (folded as in ChainStackFunction).
+    """
+
+    @staticmethod
+    def forward(ctx, x, target, M, per_shell, Bt, state_fwd, state_bwd, n_layers, *layers):
+        lib = _lib.load()
+        lays = [layers[4 * i:4 * i + 4] for i in range(n_layers)]
+        Ls, bvecs, L_tot, b_tot = _fold_layers(lays)
+        w1, f1, wn, fn = lays[0][0], lays[0][2], lays[-1][0], lays[-1][2]
+        s_in, r_in, s_out, r_out = w1.shape[1], f1.shape[2], wn.shape[0], fn.shape[1]
+        n, n_out = M.shape[-1], Bt.shape[0]
+        B, V = x.shape[0], nvox_of(x)
+        if tuple(target.shape) != (B, s_out * n_out, *x.shape[2:]):
+            raise ShapeError(f"target has shape {tuple(target.shape)}, the chain output is "
+                             f"{(B, s_out * n_out, *x.shape[2:])}")
+        target = as_device_f32(target, "target")
+        want_w = any(ctx.needs_input_grad[8:])
+        dy = torch.empty((B, s_out * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
+        loss = torch.zeros(4, dtype=torch.float64, device=x.device)
+        c_mid = _workspace(lib.dl_chain_mid_bytes(B, s_in, r_in, V), x.device) if want_w else None
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), x.device)
+        _lib.call("dl_chain_fwd_mse_f32", _p(x), _p(target), _p(dy), _p(c_mid), _p(M), int(per_shell), _p(L_tot),
+                  _p(b_tot), _p(Bt), _p(ws), _p(state_fwd), _p(loss), B, s_in, s_out, n, r_in, r_out, n_out, V,
+                  _stream())
+        ctx.save_for_backward(c_mid, dy, M, Bt, L_tot, *[t for lay in lays for t in (lay[0], lay[2], lay[3])])
+        ctx.Ls, ctx.bvecs = Ls, bvecs
+        ctx.dims = (s_in, s_out, n, r_in, r_out, n_out, B, V, tuple(x.shape), n_layers)
+        ctx.has_bias = [lay[1] is not None for lay in lays]
+        ctx.per_shell, ctx.state_bwd = per_shell, state_bwd
+        return loss[2].float()
+
+    @staticmethod
+    def backward(ctx, g):
+        c_mid, dy, M, Bt, L_tot, *lay = ctx.saved_tensors
+        s_in, s_out, n, r_in, r_out, n_out, B, V, xshape, nl = ctx.dims
+        lib = _lib.load()
+        out = [None] * (8 + 4 * nl)
+        want_x = ctx.needs_input_grad[0]
+        if ctx.needs_input_grad[1]:
+            out[1] = -dy * g
+        if c_mid is None and not want_x:
+            return tuple(out)
+        dx = torch.empty(xshape, dtype=torch.float32, device=dy.device) if want_x else None
+        ws = _workspace(lib.dl_chain_workspace_bytes(B, s_in, s_out, n, r_in, r_out, n_out, V), dy.device)
+        if c_mid is None:
+            _lib.call("dl_chain_bwd_f32", _NULL, _p(dy), _p(dx), _NULL, _NULL, _NULL, _p(M), int(ctx.per_shell),
+                      _p(L_tot), _p(Bt), _NULL, _NULL, _p(ws), _p(ctx.state_bwd), B, s_in, s_out, 1, n, r_in, r_out,
+                      n_out, V, _stream())
+        else:
+            rows, cols = ctypes.c_int64(), ctypes.c_int64()
+            _lib.call("dl_chain_gram_dims", s_in, s_out, r_in, r_out, ctypes.byref(rows), ctypes.byref(cols))
+            G = torch.empty((rows.value, cols.value), dtype=torch.float64, device=dy.device)
+            g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device)
+            _lib.call("dl_chain_bwd_gram_f64", _p(c_mid), _p(dy), _p(dx), _p(G), _p(g_mid), _p(M),
+                      int(ctx.per_shell), _p(L_tot), _p(Bt), _p(ws), _p(ctx.state_bwd), B, s_in, s_out, n, r_in, r_out,
+                      n_out, V, _stream())
+            grads = _layer_grads(G, rows.value, cols.value, (s_in, s_out, r_in, r_out, nl), ctx.Ls, ctx.bvecs, lay,
+                                 ctx.has_bias, dy.device)
+            for k in range(nl):
+                if ctx.needs_input_grad[8 + 4 * k] and grads[2 * k] is not None:
+                    out[8 + 4 * k] = grads[2 * k] * g
+                if ctx.needs_input_grad[8 + 4 * k + 1] and grads[2 * k + 1] is not None:
+                    out[8 + 4 * k + 1] = grads[2 * k + 1] * g
+        if want_x:
+            out[0] = dx * g
+        return tuple(out)
+
+
+def chain_mse_supported(s_in: int, s_out: int, n: int, r_in: int, r_out: int, n_out: int, per_shell: bool) -> bool:
+    """True if the fused-loss forward (dl_chain_fwd_mse_f32) covers these channel counts."""
+    return bool(_lib.load().dl_chain_mse_supported(s_in, s_out, n, r_in, r_out, n_out, int(per_shell)))
+
+
 def fp16_pass_enabled() -> bool:
     """True when the fused chain runs the fp16 two-term pass (the default precision mode)."""
     import os

@@ -566,3 +566,30 @@ def test_fused_chain_weight_grads_without_dx(dev, stack):
         grads.append([N(t) for m in mods for t in (m.sconv.weight.grad, m.sconv.bias.grad)])
     for a, b in zip(*grads):   # the second call runs at the re-centred fp16 scale: fp32-class agreement
         assert rel(b, a) <= 1e-5
+
+
+@pytest.mark.parametrize("stack,need_x", [(1, True), (1, False), (2, False), (2, True)])
+def test_fused_mse_loss_vs_unfused(dev, stack, need_x):
+    """SphericalChain.mse_loss fuses the loss and its gradient into the forward kernel (dy = 2 (y - t) / N in
+    place of y); the loss equals torch's MSE on the chain output to 1e-5, dx and every layer's dW / db to
+    TOL_LSC (both sides are fp32 paths through the LSC layers)."""
+    rng = np.random.default_rng(41 + stack)
+    d = unit_sphere_directions(90)
+    mods = [make_lsc(d, 3, 3, 8, 8, [5], np.pi / 5, 0.006, rng.normal(size=(3, 3, 6)) / 18, rng.normal(size=3) * 0.1,
+                     dev) for _ in range(stack)]
+    chain = dl.SphericalChain(dl.Signal2SH(8, d, lb_lambda=0.006).to(dev), mods if stack > 1 else mods[0],
+                              dl.SH2Signal(8, d).to(dev))
+    x = T(rng.uniform(0.1, 1.3, size=(1, 270, 17, 13, 6)), dev)
+    t = T(rng.uniform(0.0, 1.5, size=(1, 270, 17, 13, 6)), dev)
+    res = []
+    for fused in (True, False):
+        for m in mods:
+            m.zero_grad(set_to_none=True)
+        xi = x.clone().requires_grad_(need_x)
+        loss = chain.mse_loss(xi, t, fused=True) if fused else torch.nn.functional.mse_loss(chain(xi), t)
+        (3.0 * loss).backward()   # a non-unit upstream gradient
+        res.append([float(loss.detach())] + [N(p) for m in mods for p in (m.sconv.weight.grad, m.sconv.bias.grad)]
+                   + ([N(xi.grad)] if need_x else []))
+    assert abs(res[0][0] - res[1][0]) <= 1e-5 * abs(res[1][0])
+    for a, b in zip(res[0][1:], res[1][1:]):   # two fp32 paths through LSC layers: TOL_LSC
+        assert rel(a, b) <= TOL_LSC
