@@ -1079,17 +1079,19 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
             const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             float* d = p.out + off;
             const int nval = p.C3 - ck * 16;
-            if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
+            if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals (loads first, see chain2h)
               const float* tg = p.target + off;
+              float tv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) tv[i] = (nval >= 16 || i < nval) ? __ldcs(tg + (int64_t)i * stride) : 0.f;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 if (nval >= 16 || i < nval) {
-                  const float r = vv[i] - __ldcs(tg);
+                  const float r = vv[i] - tv[i];
                   lacc += (double)r * (double)r;
                   __stcs(d, r * p.out_scale);
                 }
                 d += stride;
-                tg += stride;
               }
             } else if (nval >= 16) {
 #pragma unroll
@@ -1479,16 +1481,24 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             const int nval = p.C3 - ck * 16;
             const float* bb = sb + o * p.N3 + ck * 16;
             if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
+              // all 16 target loads first: the stores below could alias them, so loads interleaved with
+              // stores would each wait out a full memory latency
               const float* tg = p.target + off;
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                if (nval >= 16 || e < nval) {
-                  const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - __ldcs(tg);
-                  lacc += (double)res * (double)res;
-                  __stcs(d, res * p.out_scale);
+              for (int h = 0; h < 16; h += 4) {   // four loads in flight at a time (register budget)
+                float tv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  tv[e] = (nval >= 16 || h + e < nval) ? __ldcs(tg + (int64_t)(h + e) * stride) : 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  if (nval >= 16 || h + e < nval) {
+                    const float res = fmaf(__uint_as_float(r[k][h + e]), isc, bb[h + e]) - tv[e];
+                    lacc += (double)res * (double)res;
+                    __stcs(d, res * p.out_scale);
+                  }
+                  d += stride;
                 }
-                d += stride;
-                tg += stride;
               }
             } else {
 #pragma unroll

@@ -43,7 +43,7 @@ def main(steps=20, warmup=3):
     opt = torch.optim.SGD(params, lr=1e-3)
     nvox = x[0, 0].numel()
 
-    fused = os.environ.get("CFG5_FUSED_LOSS") is not None
+    fused = os.environ.get("CFG5_UNFUSED_LOSS") is None
 
     def step():
         opt.zero_grad(set_to_none=True)
@@ -71,8 +71,8 @@ def main(steps=20, warmup=3):
                           "value": world * nvox / (ms / 1e3), "unit": "voxels/s", "n_gpus": world, "steps": steps,
                           "ms_per_step": ms, "loss": float(loss.detach()), "dtype": "f32",
                           "loss_fused": fused,
-                          "note": "torch's MSE on the chain output (CFG5_FUSED_LOSS=1: the loss inside the forward "
-                                  "kernel); x needs no gradient, so the adjoint is the g-only pass (no dx)"}))
+                          "note": "MSE loss and its gradient inside the forward kernel (CFG5_UNFUSED_LOSS=1: torch's "
+                                  "MSE on the chain output); x needs no gradient, so the adjoint is the g-only pass"}))
 
 
 if __name__ == "__main__":
