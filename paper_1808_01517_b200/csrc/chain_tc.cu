@@ -522,6 +522,10 @@ __device__ __forceinline__ bool range_check(uint32_t* st) {
   return ok;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 // warp sum of the squared residuals -> one float64 atomic per warp (fused MSE)
 __device__ __forceinline__ void loss_publish(double* acc, double v) {
 #pragma unroll
@@ -1457,6 +1461,15 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       }
       for (int o = 0; o < p.G2; ++o, ++n3) {
         const uint32_t xb = KOUT ? 0u : (n3 & 1);
+        if (p.target && vok) {   // fused MSE: pull this shell's target rows into L2 while the MMA runs
+          for (int ck = cg; ck < nck; ck += kOUTQ) {
+            const int nval = p.C3 - ck * 16;
+            const float* tg = p.target + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (nval >= 16 || e < nval) prefetch_l2(tg + (int64_t)e * stride);
+          }
+        }
         if (!KOUT) {
           idle_wait<1>(&bars.d3_full[xb], (n3 >> 1) & 1);
           fence_after();
@@ -1484,6 +1497,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
               // all 16 target loads first: the stores below could alias them, so loads interleaved with
               // stores would each wait out a full memory latency
               const float* tg = p.target + off;
+              float csum = 0.f;   // 16 squares in fp32, then one float64 add per chunk
 #pragma unroll
               for (int h = 0; h < 16; h += 4) {   // four loads in flight at a time (register budget)
                 float tv[4];
@@ -1494,12 +1508,13 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
                 for (int e = 0; e < 4; ++e) {
                   if (nval >= 16 || h + e < nval) {
                     const float res = fmaf(__uint_as_float(r[k][h + e]), isc, bb[h + e]) - tv[e];
-                    lacc += (double)res * (double)res;
+                    csum = fmaf(res, res, csum);
                     __stcs(d, res * p.out_scale);
                   }
                   d += stride;
                 }
               }
+              lacc += (double)csum;
             } else {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
