@@ -161,6 +161,9 @@ __device__ __forceinline__ void store16(float* d, int64_t stride, const float (&
   }
 }
 
+__device__ __forceinline__ void st_cs_u32(uint16_t* p, uint32_t v) {
+  asm volatile("st.global.cs.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_cs_u16(uint16_t* p, uint32_t v) {
   asm volatile("st.global.cs.u16 [%0], %1;\n" ::"l"(p), "h"((unsigned short)v) : "memory");
 }
@@ -170,15 +173,23 @@ __device__ __forceinline__ void st_cs_u16(uint16_t* p, uint32_t v) {
 // is stored as exactly 1.0: a zero-weight padding row whose Gram column sums g (the bias gradient).
 __device__ __forceinline__ void store_mid(uint16_t* d, int64_t plane, int64_t pitch, const uint32_t (&w0)[8],
                                           const uint32_t (&w1)[8], int ones) {
+  // Lanes (2j, 2j+1) hold adjacent voxels: they trade their packed row pairs so that the even lane stores
+  // row 2i and the odd lane row 2i+1 of both voxels as one 32-bit word -- half the store instructions of
+  // per-voxel 16-bit stores.  Callers are warp-uniform (whole warps inside or outside the mid buffer).
+  const uint32_t odd = threadIdx.x & 1u;
+  uint16_t* base = d - odd;   // the pair's first voxel (4-byte aligned: tiles are 64 voxels)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     uint32_t a = w0[i], c = w1[i];
     if (2 * i == ones) { a = (a & 0xFFFF0000u) | 0x3F80u; c &= 0xFFFF0000u; }
     if (2 * i + 1 == ones) { a = (a & 0x0000FFFFu) | 0x3F800000u; c &= 0x0000FFFFu; }
-    st_cs_u16(d + (int64_t)(2 * i) * pitch, a & 0xFFFFu);
-    st_cs_u16(d + (int64_t)(2 * i + 1) * pitch, a >> 16);
-    st_cs_u16(d + plane + (int64_t)(2 * i) * pitch, c & 0xFFFFu);
-    st_cs_u16(d + plane + (int64_t)(2 * i + 1) * pitch, c >> 16);
+    const uint32_t pa = __shfl_xor_sync(0xffffffffu, a, 1), pc = __shfl_xor_sync(0xffffffffu, c, 1);
+    const uint32_t sel_lo = odd ? 0x7632u : 0x5410u;
+    const uint32_t wa = odd ? __byte_perm(pa, a, sel_lo) : __byte_perm(a, pa, sel_lo);
+    const uint32_t wc = odd ? __byte_perm(pc, c, sel_lo) : __byte_perm(c, pc, sel_lo);
+    uint16_t* r = base + (int64_t)(2 * i + (int)odd) * pitch;
+    st_cs_u32(r, wa);
+    st_cs_u32(r + plane, wc);
   }
 }
 
