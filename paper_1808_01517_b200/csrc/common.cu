@@ -67,7 +67,7 @@ int device_check(int* sm_count) {
 
 extern "C" {
 
-int dl_abi_version(void) { return 102; }
+int dl_abi_version(void) { return 103; }
 
 const char* dl_last_error(void) { return g_err; }
 
