@@ -380,7 +380,11 @@ def run_ours(args):
                          "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": dom[1], "launch_ms": dom[2],
-                         "bytes_per_voxel": 2160, "traffic": ncu_traffic(dom[0])},
+                         "bytes_per_voxel": 2160, "traffic": ncu_traffic(dom[0]),
+                         # DRAM bytes the launch actually moves (algorithmic x + y plus the Gram term planes,
+                         # profiles/ncu_traffic.json) over the same time: how close the memory system runs
+                         "dram_gbs": (ncu_traffic(dom[0]) or 0) / (dom[2] / 1e3) / 1e9 or None,
+                         "dram_frac": ((ncu_traffic(dom[0]) or 0) / (dom[2] / 1e3) / 1e9) / peak or None},
             "phase_ms": {"fwd": fwd_ms, "bwd": bwd_ms},
             "step_hbm_gbs": (fwd_bytes + bwd_bytes) / (ms / 1e3) / 1e9,
             "cpu_baseline": cpu,
