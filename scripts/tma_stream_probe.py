@@ -15,5 +15,7 @@ for rows in (144, 288):
     print(f"reads only, 1 consumer warp,  rows={rows}: {ms.value:.3f} ms {gb/ms.value:.2f} TB/s")
     lib.tma_stream_rw(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), nvox, rows, 8, 0, ctypes.byref(ms))
     print(f"reads only, 4 consumer warps, rows={rows}: {ms.value:.3f} ms {gb/ms.value:.2f} TB/s")
+    lib.tma_stream_rw(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), nvox, rows, 8, -1, ctypes.byref(ms))
+    print(f"reads only, 4 warps, LDS.128 row-wise, rows={rows}: {ms.value:.3f} ms {gb/ms.value:.2f} TB/s")
     lib.tma_stream_rw(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), nvox, rows, 8, 16, ctypes.byref(ms))
     print(f"read+write,  4 consumer warps, rows={rows}: {ms.value:.3f} ms {2*gb/ms.value:.2f} TB/s")
