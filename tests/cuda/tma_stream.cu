@@ -100,25 +100,13 @@ __global__ void __launch_bounds__(160, 1) stream_rw_k(const __grid_constant__ P 
       const int64_t v = t * p.W + 32 * q + lane;
       for (int r = 0; r < per_tile; ++r) {
         mbar_wait_warp(&full[s], round & 1);
+        const float* rp = reinterpret_cast<const float*>(ring + s * stage) + 32 * q + lane;
         float vals[16];
-        if (wrows < 0) {   // row-wise variant: warp q reads rows 4q..4q+3, each as one LDS.128 per lane
-          const float* rb = reinterpret_cast<const float*>(ring + s * stage);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int rr = 4 * q + j;
-            const float4 f4 = *reinterpret_cast<const float4*>(rb + (rr & 1) * 8 * (p.W + 4) + (rr >> 1) * (p.W + 4) + 4 * lane);
-            vals[4 * j] = f4.x; vals[4 * j + 1] = f4.y; vals[4 * j + 2] = f4.z; vals[4 * j + 3] = f4.w;
-          }
-        } else {
-          const float* rp = reinterpret_cast<const float*>(ring + s * stage) + 32 * q + lane;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) vals[j] = rp[(j & 1) * odd0 + (j >> 1) * (p.W + 4)];
-        }
+        for (int j = 0; j < 16; ++j) vals[j] = rp[(j & 1) * odd0 + (j >> 1) * (p.W + 4)];
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (wrows < 0) {
-          if (vals[0] == 12345.f && vals[15] == 1.f) out[0] = vals[3];   // keep the reads
-        } else if (v < p.nvox) {
+        if (v < p.nvox) {
           float* d = out + (int64_t)(16 * r) * p.nvox + v;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
