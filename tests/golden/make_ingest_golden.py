@@ -11,6 +11,7 @@ Writes tests/golden/ingest/:
   kernel_ref.json  a 2 -> 3 shell, two-ring LSC kernel written by the reference's lsc.save_kernel_json
   cli_sh.nii.gz, cli_lsc.nii.gz, cli_sig.nii.gz  the reference CLI's signal2sh (order 4) / lsc (moving
                 average 5 at pi/5) / sh2signal (shell 1000 directions) outputs on acq.nii.gz
+  cli_lsc_k.nii.gz  the reference CLI's lsc with kernel_ref.json (2 -> 3 shells, rings [5, 7]) to order 2
   expected.npz  reference outputs: read_nifti data (float64, slope applied), normalize_b0 on the file's data
                 (all shells; shell 2000 only) with the exclusion mask, and normalize_b0 of an in-memory float64
                 array with a zero-b0 voxel.
@@ -74,6 +75,8 @@ def main():
                 "--out", j("cli_lsc.nii.gz")]) == 0
     assert cli(["sh2signal", "--sh", j("cli_lsc.nii.gz"), *g, "--shell", "1000", "--order", "4",
                 "--out", j("cli_sig.nii.gz")]) == 0
+    assert cli(["lsc", "--sh", j("cli_sh.nii.gz"), *g, "--kernel", j("kernel_ref.json"), "--order-out", "2",
+                "--out", j("cli_lsc_k.nii.gz")]) == 0
     print("wrote", OUT, vol.data.shape, int(mask.sum()), vol3.data.shape, int(mask3.sum()))
 
 

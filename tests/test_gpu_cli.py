@@ -73,3 +73,11 @@ def test_cli_bench_csv(tmp_path):
     for ln in lines[1:]:
         d, o, v, m, s, dev = ln.split(",")
         assert m in ("gpu", "gpu-e2e") and float(s) > 0 and float(dev) < 1e-4
+
+
+def test_cli_lsc_with_kernel_json(tmp_path):
+    """lsc --kernel with the reference-written kernel document (2 -> 3 shells, rings [5, 7], order 4 -> 2)."""
+    out = str(tmp_path / "lsck.nii.gz")
+    assert main(["lsc", "--sh", j("cli_sh.nii.gz"), *GR, "--kernel", j("kernel_ref.json"), "--order-out", "2",
+                 "--out", out]) == 0
+    assert port.rel_err(rd(out), rd(j("cli_lsc_k.nii.gz"))) <= 1e-4
