@@ -455,7 +455,8 @@ def test_fallback_kernels_match_oracle(env):
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_parity.py"), "-q", "-x",
-                          "-m", "gpu", "-k", "fused_chain_vs_oracle or bitwise_deterministic"],
+                          "-m", "gpu", "-k", "fused_chain_vs_oracle or bitwise_deterministic or stacked or "
+                                             "without_dx or mse_loss"],
                          env={**os.environ, **env}, capture_output=True, text=True, timeout=900, cwd=root)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
 
