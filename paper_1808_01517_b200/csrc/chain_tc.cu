@@ -1289,7 +1289,10 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 //   OUT       D3 -> y (x 2^-e + bias3) while the MMA fills the other D3 buffer.
 // Against chain3v this drops the D2 accumulator and its conversion pass (half of CONV's TMEM loads, splits
 // and handoffs) for ~14% more MMA work; it needs the T images (G2 x N3 x K2 fp16 pairs) in shared memory.
-constexpr int kOB2h = 2;   // D3 chunks an OUT warp loads before releasing / storing them
+#ifndef DL_OB2H
+#define DL_OB2H 1
+#endif
+constexpr int kOB2h = DL_OB2H;   // D3 chunks an OUT warp loads before releasing / storing them
 struct Bars2h {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
