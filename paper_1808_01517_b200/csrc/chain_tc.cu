@@ -2186,7 +2186,7 @@ bool plan_chain2h(Chain3& p, bool kout) {
   const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1;
   const int D3w = kout ? p.G2 * p.N3 : 2 * p.N3;
   int A2w = p.G1 * p.N1;
-  p.cpi = 2;
+  p.cpi = getenv("DELIMIT_IN_SINGLE") ? 1 : 2;   // measurement knob: one chunk per IN item
   if (kout) {   // two IN items, the rest A2 ring slots (>= 2)
     p.NA = 2;
     p.NAc = (512 - D1w - D3w - 2 * 2 * parts * 8) / (parts * 8);
@@ -2195,14 +2195,14 @@ bool plan_chain2h(Chain3& p, bool kout) {
     A2w = p.NAc * parts * 8;
   } else {
     const int spare = 512 - D1w - A2w - D3w;
-    p.NA = spare / (2 * parts * 8);
+    p.NA = spare / (p.cpi * parts * 8);
     if (p.NA < 2) return false;
     if (p.NA > kMaxSlots) p.NA = kMaxSlots;
     p.NAc = 0;
   }
-  if (D1w + A2w + D3w + p.NA * 2 * parts * 8 > 512) return false;
+  if (D1w + A2w + D3w + p.NA * p.cpi * parts * 8 > 512) return false;
   p.colA = 0;
-  p.colD1 = (uint32_t)(p.NA * 2 * parts * 8);
+  p.colD1 = (uint32_t)(p.NA * p.cpi * parts * 8);
   p.colA2 = p.colD1 + (uint32_t)D1w;
   p.colD3 = p.colA2 + (uint32_t)A2w;
   p.w1_img = (uint32_t)(p.N1 * p.K1 * 2);
