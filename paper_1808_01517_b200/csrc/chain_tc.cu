@@ -417,6 +417,29 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
       const uint32_t q0 = 2 * pr, cs0 = q0 % NS, cs1 = (q0 + 1) % NS;
       const ChunkGeo cg = geo(r);
       const int nval0 = vok ? cg.nval : 0, nval1 = vok ? cg.nval - 16 : 0;
+      const uint32_t ta = tslots + aslot * (2 * PARTS * 8);
+#if DL_IN_SEQ
+      // the two chunks one after the other: 16 values and their terms live at a time (register budget)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t cs = h ? cs1 : cs0;
+        const int nv = h ? nval1 : nval0;
+        float v[16];
+        idle_wait<0>(&full[cs], ((q0 + h) / NS) & 1);
+        const float* rp = ring + cs * (kStageBytes / 4) + 32 * qd + lane;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = j < nv ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+        warp_arrive(&empty[cs]);
+        scale16<H>(v, sc, am);
+        uint32_t w[PARTS][8];
+        split16<PARTS, H>(v, w);
+        if (h == 0) {
+          if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
+          fence_after();
+        }
+        store_parts<PARTS>(ta + (uint32_t)h * PARTS * 8, 8, w);
+      }
+#else
       float v0[16], v1[16];
       idle_wait<0>(&full[cs0], (q0 / NS) & 1);
       const float* rp0 = ring + cs0 * (kStageBytes / 4) + 32 * qd + lane;
@@ -435,9 +458,9 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
       split16<PARTS, H>(v1, w1);
       if (around > 0) idle_wait<0>(&a_empty[aslot], (around - 1) & 1);
       fence_after();
-      const uint32_t ta = tslots + aslot * (2 * PARTS * 8);
       store_parts<PARTS>(ta, 8, w0);
       store_parts<PARTS>(ta + PARTS * 8, 8, w1);
+#endif
       tmem_wait_st();
       fence_before();
       warp_arrive(&a_full[aslot]);
@@ -1289,6 +1312,9 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 //   OUT       D3 -> y (x 2^-e + bias3) while the MMA fills the other D3 buffer.
 // Against chain3v this drops the D2 accumulator and its conversion pass (half of CONV's TMEM loads, splits
 // and handoffs) for ~14% more MMA work; it needs the T images (G2 x N3 x K2 fp16 pairs) in shared memory.
+#ifndef DL_IN_SEQ
+#define DL_IN_SEQ 0
+#endif
 #ifndef DL_OB2H
 #define DL_OB2H 1
 #endif
