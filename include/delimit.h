@@ -179,6 +179,13 @@ int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */
 int64_t dl_total_launch_count(void);
 
+/* Kernel timer (measurement aid for bench.py; no reference counterpart): when armed, each fp16-pass launch of
+ * the fused chain kernel is bracketed by CUDA events on its own stream (slot 0 forward, 1 adjoint); under
+ * stream capture they become external event nodes that every graph replay re-records.  dl_ktimer_read returns
+ * the last bracketed launch's duration in ms once the stream has passed it. */
+int dl_ktimer_arm(int on);
+int dl_ktimer_read(int slot, float* ms);
+
 /* Debug hook (not part of the stable ABI): record chain phase timestamps of CTA 0. */
 void dl_debug_chain_prof(void* buf);
 

@@ -40,6 +40,8 @@ SIGNATURES = {
     "dl_chain_fwd_f32": (_int, [_c_p, _c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p, _c_p, _c_p] + [_i64] * 8 + [_c_p]),
     "dl_chain_bwd_f32": (_int, [_c_p] * 7 + [_int] + [_c_p] * 6 + [_i64] * 9 + [_c_p]),
     "dl_debug_chain_prof": (None, [_c_p]),
+    "dl_ktimer_arm": (_int, [_int]),
+    "dl_ktimer_read": (_int, [_int, _c_p]),
     "dl_chain_bwd_gram_f64": (_int, [_c_p] * 6 + [_int] + [_c_p] * 4 + [_i64] * 8 + [_c_p]),
     "dl_chain_gram_dims": (_int, [_i64] * 4 + [_c_p, _c_p]),
     "dl_chain_fwd_mse_f32": (_int, [_c_p] * 5 + [_int] + [_c_p] * 6 + [_i64] * 8 + [_c_p]),
@@ -89,6 +91,18 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().dl_last_launch_count())
+
+
+def ktimer_arm(on: bool = True) -> None:
+    """Bracket the fused chain kernel's fp16-pass launches with CUDA events (see dl_ktimer_arm)."""
+    call("dl_ktimer_arm", int(on))
+
+
+def ktimer_read(slot: int) -> float:
+    """Duration (ms) of the last bracketed chain launch: slot 0 forward, 1 adjoint."""
+    ms = ctypes.c_float()
+    call("dl_ktimer_read", slot, ctypes.byref(ms))
+    return float(ms.value)
 
 
 def total_launches() -> int:

@@ -2335,9 +2335,12 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
       h2.bias2 = bias3;
       h2.rstate = rstate;
       h2.redo = 0;
+      const int slot = what[6] == 'f' ? 0 : 1;   // "chain_fwd" / "chain_bwd"
+      DL_TRY(ktimer_record(slot, 0, st));
       if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
       else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));
       else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
+      DL_TRY(ktimer_record(slot, 1, st));
       v.rstate = rstate;
       v.redo = 1;
       v.prof = nullptr;

@@ -12,6 +12,9 @@ thread_local int g_launches = 0;
 std::atomic<int64_t> g_total_launches{0};
 int g_sm_count[64] = {0};   // per device ordinal, 0 = unknown
 int g_supported[64] = {0};  // 1 ok, -1 unsupported, 0 unknown
+// kernel timer (dl_ktimer_*): [slot][begin / end]
+bool g_kt_armed = false;
+cudaEvent_t g_kt_ev[2][2] = {};
 }  // namespace
 
 namespace dl {
@@ -63,9 +66,35 @@ int device_check(int* sm_count) {
   return DL_OK;
 }
 
+int ktimer_record(int slot, int end, cudaStream_t st) {
+  if (!g_kt_armed || slot < 0 || slot > 1) return DL_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DL_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive)   // an external event node: every graph replay re-records it
+    DL_CUDA(cudaEventRecordWithFlags(g_kt_ev[slot][end], st, cudaEventRecordExternal));
+  else
+    DL_CUDA(cudaEventRecord(g_kt_ev[slot][end], st));
+  return DL_OK;
+}
+
 }  // namespace dl
 
 extern "C" {
+
+int dl_ktimer_arm(int on) {
+  if (on && !g_kt_ev[0][0])
+    for (auto& pair : g_kt_ev)
+      for (auto& ev : pair) DL_CUDA(cudaEventCreate(&ev));
+  g_kt_armed = on != 0;
+  return DL_OK;
+}
+
+int dl_ktimer_read(int slot, float* ms) {
+  DL_REQUIRE(slot == 0 || slot == 1, "ktimer_read: slot %d (0 forward, 1 adjoint)", slot);
+  DL_REQUIRE(ms && g_kt_ev[slot][0], "ktimer_read: timer never armed or null output");
+  DL_CUDA(cudaEventElapsedTime(ms, g_kt_ev[slot][0], g_kt_ev[slot][1]));
+  return DL_OK;
+}
 
 int dl_abi_version(void) { return 103; }
 

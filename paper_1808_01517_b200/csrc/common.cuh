@@ -18,6 +18,9 @@ void begin_call();
 // Validate the current device is sm_100 and return its SM count (cached per device).
 int device_check(int* sm_count);
 
+// Kernel timer: when armed (dl_ktimer_arm), record slot's begin (end = 0) or end event on st.
+int ktimer_record(int slot, int end, cudaStream_t st);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 template <typename T>
