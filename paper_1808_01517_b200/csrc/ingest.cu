@@ -111,6 +111,10 @@ __global__ void mask_k(Geo g, const double* __restrict__ mean, const double* __r
 // channels; the tile's float64 b0 means are staged in shared memory once and reused for every channel.
 // Grid: (ceil(X / 32), ceil(Z / 32), Y * ceil(n_sel / kKB)); block 32 x 8.
 constexpr int kKB = 48;
+#ifndef DL_INGEST_PRE
+#define DL_INGEST_PRE 2
+#endif
+constexpr int kPre = DL_INGEST_PRE;   // channels of raw values a thread keeps in flight
 template <typename T>
 __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, Geo g, double slope, double inter,
                                                   const int64_t* __restrict__ sel, int n_sel,
@@ -148,10 +152,10 @@ __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, 
   }
   const T* base = reinterpret_cast<const T*>(raw) + y * g.sy;
   const int64_t k1 = k0 + kKB < n_sel ? k0 + kKB : n_sel;
-  // Raw values are loaded two channels ahead (registers) and transposed through a double-buffered
-  // shared-memory tile in their stored type, so a block keeps three channels' reads in flight and meets
+  // Raw values are loaded kPre channels ahead (registers) and transposed through a double-buffered
+  // shared-memory tile in their stored type, so a block keeps kPre + 1 channels' reads in flight and meets
   // one barrier per channel.
-  T pa[kT / 8], pb[kT / 8];
+  T pf[kPre][kT / 8];   // channels k + 1 ... k + kPre, oldest first
   auto load = [&](int64_t k, T (&dst)[kT / 8]) {
     const T* src = base + __ldg(sel + k) * g.sv;
 #pragma unroll
@@ -160,16 +164,18 @@ __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, 
       dst[q] = (x < X && z < Z) ? src[x + z * sz] : (T)0;
     }
   };
-  if (k0 < k1) load(k0, pa);
-  if (k0 + 1 < k1) load(k0 + 1, pb);
+#pragma unroll
+  for (int i = 0; i < kPre; ++i)
+    if (k0 + i < k1) load(k0 + i, pf[i]);
   for (int64_t k = k0; k < k1; ++k) {
     const int buf = (int)((k - k0) & 1);
 #pragma unroll
     for (int q = 0; q < kT / 8; ++q) {
-      tile[buf][ty + 8 * q][tx] = pa[q];
-      pa[q] = pb[q];
+      tile[buf][ty + 8 * q][tx] = pf[0][q];
+#pragma unroll
+      for (int i = 0; i + 1 < kPre; ++i) pf[i][q] = pf[i + 1][q];
     }
-    if (k + 2 < k1) load(k + 2, pb);
+    if (k + kPre < k1) load(k + kPre, pf[kPre - 1]);
     __syncthreads();
     float* ok = out + k * nvox;
 #pragma unroll
