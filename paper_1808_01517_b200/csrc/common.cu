@@ -96,7 +96,7 @@ int dl_ktimer_read(int slot, float* ms) {
   return DL_OK;
 }
 
-int dl_abi_version(void) { return 103; }
+int dl_abi_version(void) { return 104; }
 
 const char* dl_last_error(void) { return g_err; }
 
