@@ -305,9 +305,10 @@ def run_ours(args):
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bwd_ev)
     # The dominant kernel's own launch duration: CUDA events that dl_ktimer_* records on the kernel's stream
-    # around each fused-chain launch.  Read after K eager steps run after the timed region (same kernels, inputs
-    # and buffers), each read once the stream has passed it.  (Event nodes captured inside the graphs read
-    # longer than the whole forward phase, so the graphs stay uninstrumented.)
+    # around each fused-chain launch, over K eager steps run right after the timed region (same kernels, inputs
+    # and buffers), each read once the stream has passed it.  Measured alternatives, both noisier: event nodes
+    # captured inside the graphs read longer than the whole forward phase, and eager steps run back to back
+    # without the per-step synchronize spread 2.0-2.7 ms per launch.
     kern = None
     try:
         _lib.ktimer_arm(True)
@@ -317,8 +318,10 @@ def run_ours(args):
             torch.cuda.synchronize()
             kf.append(_lib.ktimer_read(0))
             kb.append(_lib.ktimer_read(1))
-        kern = {"fwd_ms": statistics.mean(kf), "bwd_ms": statistics.mean(kb), "samples": len(kf),
-                "how": "CUDA events around the chain2h_tc launch on its stream, eager steps after the timed region"}
+        kern = {"fwd_ms": statistics.median(kf), "bwd_ms": statistics.median(kb), "samples": len(kf),
+                "fwd_ms_min_max": [min(kf), max(kf)], "bwd_ms_min_max": [min(kb), max(kb)],
+                "how": "median of CUDA events around the chain2h_tc launch on its stream, one eager step at a time "
+                       "after the timed region"}
     except Exception as exc:   # a non-default kernel selection (no fp16 chain2h pass): fall back to the phase
         log(f"kernel timer unavailable ({exc}); roofline uses the forward phase time")
     finally:

@@ -180,11 +180,13 @@ int dl_last_launch_count(void);
 int64_t dl_total_launch_count(void);
 
 /* Kernel timer (measurement aid for bench.py; no reference counterpart): when armed, each fp16-pass launch of
- * the fused chain kernel is bracketed by CUDA events on its own stream (slot 0 forward, 1 adjoint); under
- * stream capture they become external event nodes that every graph replay re-records.  dl_ktimer_read returns
- * the last bracketed launch's duration in ms once the stream has passed it. */
+ * the fused chain kernel is bracketed by a pair of CUDA events on its own stream (slot 0 forward, 1 adjoint),
+ * taken from a per-slot ring of 64 pairs; under stream capture they become external event nodes that every
+ * graph replay re-records.  dl_ktimer_count: launches bracketed so far in a slot.  dl_ktimer_read: duration in
+ * ms of the launch `back` places before the last one (0 = the last), once the stream has passed it. */
 int dl_ktimer_arm(int on);
-int dl_ktimer_read(int slot, float* ms);
+int64_t dl_ktimer_count(int slot);
+int dl_ktimer_read(int slot, int back, float* ms);
 
 /* Debug hook (not part of the stable ABI): record chain phase timestamps of CTA 0. */
 void dl_debug_chain_prof(void* buf);

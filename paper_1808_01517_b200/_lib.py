@@ -41,7 +41,8 @@ SIGNATURES = {
     "dl_chain_bwd_f32": (_int, [_c_p] * 7 + [_int] + [_c_p] * 6 + [_i64] * 9 + [_c_p]),
     "dl_debug_chain_prof": (None, [_c_p]),
     "dl_ktimer_arm": (_int, [_int]),
-    "dl_ktimer_read": (_int, [_int, _c_p]),
+    "dl_ktimer_count": (_i64, [_int]),
+    "dl_ktimer_read": (_int, [_int, _int, _c_p]),
     "dl_chain_bwd_gram_f64": (_int, [_c_p] * 6 + [_int] + [_c_p] * 4 + [_i64] * 8 + [_c_p]),
     "dl_chain_gram_dims": (_int, [_i64] * 4 + [_c_p, _c_p]),
     "dl_chain_fwd_mse_f32": (_int, [_c_p] * 5 + [_int] + [_c_p] * 6 + [_i64] * 8 + [_c_p]),
@@ -98,10 +99,15 @@ def ktimer_arm(on: bool = True) -> None:
     call("dl_ktimer_arm", int(on))
 
 
-def ktimer_read(slot: int) -> float:
-    """Duration (ms) of the last bracketed chain launch: slot 0 forward, 1 adjoint."""
+def ktimer_count(slot: int) -> int:
+    """Chain launches bracketed so far in a slot (0 forward, 1 adjoint)."""
+    return int(load().dl_ktimer_count(slot))
+
+
+def ktimer_read(slot: int, back: int = 0) -> float:
+    """Duration (ms) of a bracketed chain launch: slot 0 forward, 1 adjoint; back = 0 is the last one."""
     ms = ctypes.c_float()
-    call("dl_ktimer_read", slot, ctypes.byref(ms))
+    call("dl_ktimer_read", slot, back, ctypes.byref(ms))
     return float(ms.value)
 
 

@@ -12,9 +12,11 @@ thread_local int g_launches = 0;
 std::atomic<int64_t> g_total_launches{0};
 int g_sm_count[64] = {0};   // per device ordinal, 0 = unknown
 int g_supported[64] = {0};  // 1 ok, -1 unsupported, 0 unknown
-// kernel timer (dl_ktimer_*): [slot][begin / end]
+// kernel timer (dl_ktimer_*): per slot a ring of (begin, end) event pairs, one pair per bracketed launch
+constexpr int kKtRing = 64;
 bool g_kt_armed = false;
-cudaEvent_t g_kt_ev[2][2] = {};
+cudaEvent_t g_kt_ev[2][kKtRing][2] = {};
+int64_t g_kt_n[2] = {0, 0};   // launches bracketed per slot (the ring holds the last kKtRing)
 }  // namespace
 
 namespace dl {
@@ -70,10 +72,12 @@ int ktimer_record(int slot, int end, cudaStream_t st) {
   if (!g_kt_armed || slot < 0 || slot > 1) return DL_OK;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   DL_CUDA(cudaStreamIsCapturing(st, &cs));
+  cudaEvent_t ev = g_kt_ev[slot][g_kt_n[slot] % kKtRing][end];
   if (cs == cudaStreamCaptureStatusActive)   // an external event node: every graph replay re-records it
-    DL_CUDA(cudaEventRecordWithFlags(g_kt_ev[slot][end], st, cudaEventRecordExternal));
+    DL_CUDA(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
   else
-    DL_CUDA(cudaEventRecord(g_kt_ev[slot][end], st));
+    DL_CUDA(cudaEventRecord(ev, st));
+  if (end) ++g_kt_n[slot];
   return DL_OK;
 }
 
@@ -82,17 +86,23 @@ int ktimer_record(int slot, int end, cudaStream_t st) {
 extern "C" {
 
 int dl_ktimer_arm(int on) {
-  if (on && !g_kt_ev[0][0])
-    for (auto& pair : g_kt_ev)
-      for (auto& ev : pair) DL_CUDA(cudaEventCreate(&ev));
+  if (on && !g_kt_ev[0][0][0])
+    for (auto& ring : g_kt_ev)
+      for (auto& pair : ring)
+        for (auto& ev : pair) DL_CUDA(cudaEventCreate(&ev));
   g_kt_armed = on != 0;
   return DL_OK;
 }
 
-int dl_ktimer_read(int slot, float* ms) {
+int64_t dl_ktimer_count(int slot) { return slot == 0 || slot == 1 ? g_kt_n[slot] : -1; }
+
+int dl_ktimer_read(int slot, int back, float* ms) {
   DL_REQUIRE(slot == 0 || slot == 1, "ktimer_read: slot %d (0 forward, 1 adjoint)", slot);
-  DL_REQUIRE(ms && g_kt_ev[slot][0], "ktimer_read: timer never armed or null output");
-  DL_CUDA(cudaEventElapsedTime(ms, g_kt_ev[slot][0], g_kt_ev[slot][1]));
+  DL_REQUIRE(ms && g_kt_ev[0][0][0], "ktimer_read: timer never armed or null output");
+  DL_REQUIRE(back >= 0 && back < kKtRing && back < g_kt_n[slot],
+             "ktimer_read: launch %d back of %lld bracketed (ring of %d)", back, (long long)g_kt_n[slot], kKtRing);
+  const auto& pair = g_kt_ev[slot][(g_kt_n[slot] - 1 - back) % kKtRing];
+  DL_CUDA(cudaEventElapsedTime(ms, pair[0], pair[1]));
   return DL_OK;
 }
 

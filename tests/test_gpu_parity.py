@@ -622,6 +622,14 @@ def test_kernel_timer_eager_and_graph(dev):
         torch.cuda.synchronize()
         kf, kb = _lib.ktimer_read(0), _lib.ktimer_read(1)
         assert 0 < kf <= e0.elapsed_time(e1) and kb > 0
+        n0 = _lib.ktimer_count(0)
+        for _ in range(3):   # back to back: every launch keeps its own event pair
+            chain(x).backward(dy)
+        torch.cuda.synchronize()
+        assert _lib.ktimer_count(0) == n0 + 3 and _lib.ktimer_count(1) >= 3
+        assert all(_lib.ktimer_read(0, i) > 0 for i in range(3))
+        with pytest.raises(dl.DeviceError):
+            _lib.ktimer_read(0, 64)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
