@@ -1892,8 +1892,22 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
 // `ng` row-major fp32 matrices of (nrb*rb) x (ncb*cb) -> PARTS bf16 images each of (nrb*rbp) x (ncb*cbp)
 // in the core-matrix blocked layout, image (q, g) at (q * ng + g) * img_elems.  Padding is zero.
 // out_h (optional): the same images as two fp16 terms (the fp16 chain pass).
-__global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, uint16_t* __restrict__ out_h, int ng,
-                       int nrb, int rb, int rbp, int ncb, int cb, int cbp, int parts) {
+struct PackJob {
+  const float* W;
+  uint16_t* out;
+  uint16_t* out_h;
+  int ng, nrb, rb, rbp, ncb, cb, cbp, parts;
+};
+struct PackJobs {
+  PackJob j[3];
+};
+
+__device__ __forceinline__ void pack_job(const PackJob& jb) {
+  const float* __restrict__ W = jb.W;
+  uint16_t* __restrict__ out = jb.out;
+  uint16_t* __restrict__ out_h = jb.out_h;
+  const int ng = jb.ng, nrb = jb.nrb, rb = jb.rb, rbp = jb.rbp, ncb = jb.ncb, cb = jb.cb, cbp = jb.cbp;
+  const int parts = jb.parts;
   const int R = nrb * rbp, C = ncb * cbp;
   const int64_t img = (int64_t)R * C;
   const int64_t n = img * ng;
@@ -1921,6 +1935,9 @@ __global__ void pack_k(const float* __restrict__ W, uint16_t* __restrict__ out, 
     }
   }
 }
+
+// one launch packs up to three operator images (blockIdx.y = job)
+__global__ void pack_k(PackJobs jobs) { pack_job(jobs.j[blockIdx.y]); }
 
 // Folded stage-2 operator of chain2h (float64 accumulation, fp32 result):
 //   forward  T[(o, n), (s, r)] = sum_q B'[n, q] L[(o, q), (s, r)],   bias3[(o, n)] = sum_q B'[n, q] bvec[(o, q)]
@@ -2378,33 +2395,52 @@ int run_gram(const GramP& p, int grid, cudaStream_t st) {
   }
 }
 
-int pack(const float* W, uint16_t* out, uint16_t* out_h, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp,
-         int parts, cudaStream_t st) {
-  const int64_t n = (int64_t)ng * nrb * rbp * ncb * cbp;
+PackJob pack_job_of(const float* W, uint16_t* out, uint16_t* out_h, int ng, int nrb, int rb, int rbp, int ncb, int cb,
+                    int cbp, int parts) {
+  return PackJob{W, out, out_h, ng, nrb, rb, rbp, ncb, cb, cbp, parts};
+}
+
+int pack_jobs(const PackJobs& jobs, int njobs, cudaStream_t st) {
+  if (njobs == 0) return DL_OK;
+  int64_t n = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const PackJob& j = jobs.j[i];
+    const int64_t ni = (int64_t)j.ng * j.nrb * j.rbp * j.ncb * j.cbp;
+    n = ni > n ? ni : n;
+  }
   const int blocks = (int)((n + 255) / 256 < 2048 ? (n + 255) / 256 : 2048);
-  pack_k<<<blocks, 256, 0, st>>>(W, out, out_h, ng, nrb, rb, rbp, ncb, cb, cbp, parts);
+  pack_k<<<dim3(blocks, njobs), 256, 0, st>>>(jobs);
   return after_launch("pack_operand");
 }
 
-// bf16 images (d.parts terms) and, for the fp16 pass, the fp16 two-term images
+int pack(const float* W, uint16_t* out, uint16_t* out_h, int ng, int nrb, int rb, int rbp, int ncb, int cb, int cbp,
+         int parts, cudaStream_t st) {
+  PackJobs jobs{};
+  jobs.j[0] = pack_job_of(W, out, out_h, ng, nrb, rb, rbp, ncb, cb, cbp, parts);
+  return pack_jobs(jobs, 1, st);
+}
+
+// bf16 images (d.parts terms) and, for the fp16 pass, the fp16 two-term images, in one launch
 int pack_all(const Dims& d, const WsLayout& w, uint8_t* ws, const float* M, const float* L, const float* Bt, bool h,
              cudaStream_t st) {
   auto img = [&](size_t off, size_t off_h) {
     return std::make_pair(reinterpret_cast<uint16_t*>(ws + off), h ? reinterpret_cast<uint16_t*>(ws + off_h) : nullptr);
   };
+  PackJobs jobs{};
+  int nj = 0;
   if (M) {
     auto [o, oh] = img(w.imgM, w.imgMh);
-    DL_TRY(pack(M, o, oh, d.mg, 1, d.r_in, d.RPi, 1, d.n, d.NPi, d.parts, st));
+    jobs.j[nj++] = pack_job_of(M, o, oh, d.mg, 1, d.r_in, d.RPi, 1, d.n, d.NPi, d.parts);
   }
   if (L) {
     auto [o, oh] = img(w.imgL, w.imgLh);
-    DL_TRY(pack(L, o, oh, 1, d.s_out, d.r_out, d.RPo, d.s_in, d.r_in, d.RPi, d.parts, st));
+    jobs.j[nj++] = pack_job_of(L, o, oh, 1, d.s_out, d.r_out, d.RPo, d.s_in, d.r_in, d.RPi, d.parts);
   }
   if (Bt) {
     auto [o, oh] = img(w.imgB, w.imgBh);
-    DL_TRY(pack(Bt, o, oh, 1, 1, d.n_out, d.NPo, 1, d.r_out, d.RPo, d.parts, st));
+    jobs.j[nj++] = pack_job_of(Bt, o, oh, 1, 1, d.n_out, d.NPo, 1, d.r_out, d.RPo, d.parts);
   }
-  return DL_OK;
+  return pack_jobs(jobs, nj, st);
 }
 
 // chain2h operands: the folded operator T (and, forward, its bias) in fp32, then its fp16 two-term image
