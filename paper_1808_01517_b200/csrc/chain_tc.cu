@@ -1971,12 +1971,34 @@ __global__ void fold_t_k(const float* __restrict__ L, const float* __restrict__ 
   }
 }
 
-// fixed-order float64 reduction of the per-CTA Gram partials
-__global__ void gram_reduce_k(const float* __restrict__ partials, double* __restrict__ G, int nparts, int n) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += (double)__ldg(partials + (int64_t)q * n + e);
-    G[e] = s;
+// G[e] = sum over the gram_tc parts of partials[q][e], in float64.  Block (32, 8): lane x takes one e, row y a
+// contiguous chunk of parts (eight loads in flight); the eight chunk sums are added in chunk order, so the
+// result is fixed for a given part count (deterministic run to run).
+__global__ void __launch_bounds__(256) gram_reduce_k(const float* __restrict__ partials, double* __restrict__ G,
+                                                     int nparts, int n) {
+  __shared__ double red[8][33];
+  const int e = blockIdx.x * 32 + threadIdx.x;
+  const int per = (nparts + 7) / 8;
+  const int q0 = threadIdx.y * per, q1 = q0 + per < nparts ? q0 + per : nparts;
+  double s = 0.0;
+  if (e < n) {
+    int q = q0;
+    for (; q + 8 <= q1; q += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(partials + (int64_t)(q + j) * n + e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += (double)v[j];
+    }
+    for (; q < q1; ++q) s += (double)__ldg(partials + (int64_t)q * n + e);
+  }
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && e < n) {
+    double t = red[0][threadIdx.x];
+#pragma unroll
+    for (int c = 1; c < 8; ++c) t += red[c][threadIdx.x];
+    G[e] = t;
   }
 }
 
@@ -2767,7 +2789,7 @@ int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* d
     if (nparts == 0) {
       DL_CUDA(cudaMemsetAsync(G, 0, (size_t)GR * GC * 8, st));
     } else {
-      gram_reduce_k<<<(GR * GC + 255) / 256, 256, 0, st>>>(reinterpret_cast<float*>(ws + w.parts), G, nparts, GR * GC);
+      gram_reduce_k<<<(GR * GC + 31) / 32, dim3(32, 8), 0, st>>>(reinterpret_cast<float*>(ws + w.parts), G, nparts, GR * GC);
       DL_TRY(dl::after_launch("gram_reduce"));
     }
     if (!gram_out) {
