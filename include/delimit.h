@@ -179,11 +179,13 @@ int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */
 int64_t dl_total_launch_count(void);
 
-/* Kernel timer (measurement aid for bench.py; no reference counterpart): when armed, each fp16-pass launch of
- * the fused chain kernel is bracketed by a pair of CUDA events on its own stream (slot 0 forward, 1 adjoint),
- * taken from a per-slot ring of 64 pairs; under stream capture they become external event nodes that every
- * graph replay re-records.  dl_ktimer_count: launches bracketed so far in a slot.  dl_ktimer_read: duration in
- * ms of the launch `back` places before the last one (0 = the last), once the stream has passed it. */
+/* Kernel timer (measurement aid for bench.py; no reference counterpart): while armed, the fused chain kernel's
+ * fp16-pass launches (slot 0 forward, 1 adjoint) and the LSC weight-gradient Gram launches (slot 2) stamp the
+ * device's %globaltimer when their first CTA starts and when their last CTA ends, into a per-slot device ring
+ * of 64 launches.  The stamps are kernel arguments' work, so they record the same way eagerly and inside
+ * replayed CUDA graphs, and they time the kernel alone.  dl_ktimer_count: launches recorded so far in a slot.
+ * dl_ktimer_read: duration in ms of the launch `back` places before the last one (0 = the last; back < 63).
+ * Both synchronize the device. */
 int dl_ktimer_arm(int on);
 int64_t dl_ktimer_count(int slot);
 int dl_ktimer_read(int slot, int back, float* ms);

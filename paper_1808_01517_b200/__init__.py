@@ -43,7 +43,7 @@ from .geometry import (
     sh_index,
     tangent_basis,
 )
-from .modules import LocalSphericalConvolution, SH2Signal, Signal2SH, SphericalChain, SphericalKernel
+from .modules import LocalSphericalConvolution, RoundTrip, SH2Signal, Signal2SH, SphericalChain, SphericalKernel
 from .functional import (
     DwiVolume,
     ShVolume,

@@ -100,12 +100,12 @@ def ktimer_arm(on: bool = True) -> None:
 
 
 def ktimer_count(slot: int) -> int:
-    """Chain launches bracketed so far in a slot (0 forward, 1 adjoint)."""
+    """Launches bracketed so far in a slot (0 forward chain, 1 adjoint chain, 2 Gram)."""
     return int(load().dl_ktimer_count(slot))
 
 
 def ktimer_read(slot: int, back: int = 0) -> float:
-    """Duration (ms) of a bracketed chain launch: slot 0 forward, 1 adjoint; back = 0 is the last one."""
+    """Duration (ms) of a bracketed launch: slot 0 forward chain, 1 adjoint chain, 2 Gram; back = 0 is the last."""
     ms = ctypes.c_float()
     call("dl_ktimer_read", slot, back, ctypes.byref(ms))
     return float(ms.value)

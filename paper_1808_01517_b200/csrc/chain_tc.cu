@@ -508,6 +508,8 @@ struct Chain3 {
   double* loss;
   uint32_t* rstate;                   // chain3v delayed-scaling state (kState* words) or null
   int redo;                           // chain3v bf16 pass: check the fp16 pass's ranges, recompute if needed
+  dl::KTrace* kt;                     // kernel timer (dl_ktimer_*) or null, and its slot
+  int kt_slot;
 };
 
 // Delayed scaling of the fp16 chain (state words, caller-owned, zero-initialised):
@@ -1342,6 +1344,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   constexpr int PARTS = 2;
   constexpr bool H = true;
   extern __shared__ __align__(1024) uint8_t smem[];
+  ktrace_begin(p.kt, p.kt_slot);
   Bars2h& bars = *reinterpret_cast<Bars2h*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kSlotW = PARTS * 8;
@@ -1730,6 +1733,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   fence_before();
   __syncthreads();
   if (warp == kW3MMA) tmem_dealloc(tbase, 512);
+  ktrace_end(p.kt, p.kt_slot);
 }
 
 // ============================================================================ LSC weight Gram
@@ -1737,14 +1741,22 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
 // and g = B'^T dy by the adjoint, both as two-term bf16 planes (hi, next term) with rows padded per shell
 // to 16 and voxels padded to 64 (zeros).  Those planes are exactly the operands: a TMA ring streams one
 // 64-voxel tile (c hi | c lo | g hi | g lo, SWIZZLE_128B K-major: row = channel, K = voxel) per stage and
-// the MMA warp accumulates the three split products in TMEM for the whole CTA -- no conversion warps.
+// the MMA warp accumulates the three split products in TMEM -- no conversion warps.
 // c's first padding row holds 1.0, so G's column `ones` is sum_v g_v: the bias gradient comes out of
-// the same MMAs.  Epilogue: 4 warps read G once.
+// the same MMAs.
+// Accuracy: the tensor core's fp32 accumulation is not round-to-nearest, and its error grows with the
+// accumulation length (measured at cfg4: dW error 8.6e-5 with one TMEM accumulation per CTA over ~24.7k
+// voxels, halving with every halving of the run; scripts/gram_precision.py).  So the MMA accumulates only
+// kGGroup tiles into one of two TMEM accumulators, and the 4 epilogue warps drain the finished one into
+// round-to-nearest fp32 registers (lane = G row) while the MMA fills the other; the registers are written
+// once as the CTA's partial.
 constexpr int kGV = 64;                  // voxels per Gram tile (one 128-byte bf16 K atom)
+constexpr int kGGroup = 8;               // tiles per TMEM accumulation run (512 voxels)
 constexpr int kGEpi = 4;                 // epilogue warps (one per TMEM lane quadrant)
 constexpr int kGWarpMMA = kGEpi;
 constexpr int kGWarpLD = kGEpi + 1;
 constexpr int kGThreads = (kGWarpLD + 1) * 32;
+constexpr int kGAccCols = 256;           // one accumulator: block A (<= 144) | block B (16) | block C (16)
 
 struct GramP {
   CUtensorMap tm[2];         // bf16 term planes of g (0) and c (1): dims (pitch, rows, 2 terms, nbatch)
@@ -1754,18 +1766,20 @@ struct GramP {
   int ns;
   uint32_t cpart, gpart, stage_bytes;   // stage: c hi | c lo | g hi | g lo
   uint32_t sm_ring, sm_bar, smem_bytes;
-  uint32_t colGA, colGB, colGC;
+  uint32_t colGA, colGB, colGC;         // within one accumulator
+  dl::KTrace* kt;                       // kernel timer (dl_ktimer_*, slot 2) or null
 };
 
 struct BarsG {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t done;
+  uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
 
 template <int NS>
 __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ GramP p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  ktrace_begin(p.kt, 2);
   BarsG& bars = *reinterpret_cast<BarsG*>(smem + p.sm_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
@@ -1773,13 +1787,16 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
     uint4* z = reinterpret_cast<uint4*>(smem + p.sm_ring);
     for (uint32_t i = threadIdx.x; i < NS * p.stage_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
-  if (warp == kGWarpMMA) tmem_alloc(&bars.tmem_base, 256);
+  if (warp == kGWarpMMA) tmem_alloc(&bars.tmem_base, 2 * kGAccCols);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars.full[s], 1);
       mbar_init(&bars.empty[s], 1);
     }
-    mbar_init(&bars.done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.acc_full[b], 1);
+      mbar_init(&bars.acc_empty[b], kGEpi);
+    }
     mbar_fence_init();
   }
   fence_proxy_async();
@@ -1788,6 +1805,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
   fence_after();
   const uint32_t tbase = bars.tmem_base;
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
+  const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+  const uint32_t ngroups = (nmine + kGGroup - 1) / kGGroup;
 
   if (warp == kGWarpLD) {
     // =========================== TMA loader ===========================
@@ -1818,8 +1837,14 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
     const uint32_t idA = idesc_bf16(128, p.GC, 0, 0), idB = idesc_bf16(128, 16, 0, 0), idC = idesc_bf16(64, 16, 0, 0);
     const uint32_t ring = smem_u32(smem + p.sm_ring);
     uint32_t s = 0, round = 0;
-    bool first = true;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint32_t it = 0; it < nmine; ++it) {
+      const uint32_t gi = it / kGGroup, buf = gi & 1;
+      const bool first = it % kGGroup == 0;
+      if (first && gi >= 2) {   // the epilogue has drained this accumulator's previous run
+        mbar_wait_warp(&bars.acc_empty[buf], ((gi >> 1) - 1) & 1);
+        fence_after();
+      }
+      const uint32_t acc0 = tbase + buf * kGAccCols;
       mbar_wait_warp(&bars.full[s], round & 1);
       fence_after();
       const uint32_t c0 = ring + s * p.stage_bytes, g0 = c0 + 2 * p.cpart;
@@ -1831,61 +1856,91 @@ __global__ void __launch_bounds__(kGThreads, 1) gram_tc(const __grid_constant__ 
             const uint32_t gI = g0 + (uint32_t)i * p.gpart + kk * 32u, gJ = g0 + (uint32_t)j * p.gpart + kk * 32u;
             const uint32_t cI = c0 + (uint32_t)i * p.cpart + kk * 32u, cJ = c0 + (uint32_t)j * p.cpart + kk * 32u;
             const uint32_t acc = (!first || kk > 0 || k > 0) ? 1u : 0u;
-            mma_ss(tbase + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
+            mma_ss(acc0 + p.colGA, desc_sw128_k(gI, 1024), desc_sw128_k(cJ, 1024), idA, acc);
             if (p.GR > 128) {
-              mma_ss(tbase + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
+              mma_ss(acc0 + p.colGB, desc_sw128_k(cI, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idB, acc);
               if (p.GC > 128)
-                mma_ss(tbase + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC,
+                mma_ss(acc0 + p.colGC, desc_sw128_k(cI + 16 * 1024, 1024), desc_sw128_k(gJ + 16 * 1024, 1024), idC,
                        acc);
             }
           }
         }
         __syncwarp();
       }
-      if (elect_one()) commit(&bars.empty[s]);
+      if (elect_one()) {
+        commit(&bars.empty[s]);
+        if (it % kGGroup == kGGroup - 1 || it + 1 == nmine) commit(&bars.acc_full[buf]);
+      }
       __syncwarp();
-      first = false;
       if (++s == NS) {
         s = 0;
         ++round;
       }
     }
-    if (elect_one()) commit(&bars.done);
-    __syncwarp();
   } else {
-    // =========================== epilogue: this CTA's Gram partial ===========================
-    mbar_wait_warp(&bars.done, 0);
-    fence_after();
-    const bool any = ntiles > (int64_t)blockIdx.x;
+    // =========================== epilogue: drain each run into fp32 registers, then the CTA's partial ===========
     const int qd = warp & 3, row = 32 * qd + lane;
     const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
-    float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
-    for (int ck = 0; ck < p.GC / 16; ++ck) {   // block A: lane = g row, column = c row
-      float vv[16];
-      ld16f(tq + p.colGA + (uint32_t)ck * 16, vv);
-      if (row < p.GR)
+    const int nck = p.GC / 16;
+    float ga[9][16], gb[16], gc[16];   // block A row (lane = g row), block B (lane = c row), block C
 #pragma unroll
-        for (int i = 0; i < 16; ++i) part[(int64_t)row * p.GC + ck * 16 + i] = any ? vv[i] : 0.f;
-    }
-    if (p.GR > 128) {
-      float vv[16];
-      ld16f(tq + p.colGB, vv);   // block B: lane = c row i (< 128), column = g row 128 + c
-      if (row < p.GC)
+    for (int c = 0; c < 9; ++c)
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + row] = any ? vv[c] : 0.f;
-      if (p.GC > 128 && qd == 0) {
-        ld16f(tq + p.colGC, vv);   // block C (M = 64): lanes 0..15 = c rows 128..143
-        if (lane < 16 && 128 + lane < p.GC)
+      for (int e = 0; e < 16; ++e) ga[c][e] = 0.f;
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (128 + c < p.GR) part[(int64_t)(128 + c) * p.GC + 128 + lane] = any ? vv[c] : 0.f;
+    for (int e = 0; e < 16; ++e) gb[e] = gc[e] = 0.f;
+    for (uint32_t gi = 0; gi < ngroups; ++gi) {
+      const uint32_t buf = gi & 1, acc0 = tq + buf * kGAccCols;
+      mbar_wait_warp(&bars.acc_full[buf], (gi >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        if (c < nck) {
+          uint32_t r[16];
+          tmem_ld<16>(acc0 + p.colGA + (uint32_t)c * 16, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ga[c][e] += __uint_as_float(r[e]);
+        }
       }
+      if (p.GR > 128) {
+        uint32_t r[16];
+        tmem_ld<16>(acc0 + p.colGB, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) gb[e] += __uint_as_float(r[e]);
+        if (p.GC > 128) {   // block C (M = 64) lives in lanes 0..15 of quadrant 0; every warp loads (aligned)
+          tmem_ld<16>(acc0 + p.colGC, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) gc[e] += __uint_as_float(r[e]);
+        }
+      }
+      fence_before();
+      warp_arrive(&bars.acc_empty[buf]);
+    }
+    float* part = p.partials + (int64_t)blockIdx.x * p.GR * p.GC;
+    if (row < p.GR)   // block A: lane = g row, column = c row
+#pragma unroll
+      for (int c = 0; c < 9; ++c)
+        if (c < nck)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) part[(int64_t)row * p.GC + c * 16 + e] = ga[c][e];
+    if (p.GR > 128) {
+      if (row < p.GC)   // block B: lane = c row i (< 128), column = g row 128 + e
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (128 + e < p.GR) part[(int64_t)(128 + e) * p.GC + row] = gb[e];
+      if (p.GC > 128 && qd == 0 && lane < 16 && 128 + lane < p.GC)   // block C: lanes 0..15 = c rows 128..143
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (128 + e < p.GR) part[(int64_t)(128 + e) * p.GC + 128 + lane] = gc[e];
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == kGWarpMMA) tmem_dealloc(tbase, 256);
+  if (warp == kGWarpMMA) tmem_dealloc(tbase, 2 * kGAccCols);
+  ktrace_end(p.kt, 2);
 }
 
 // ---------------------------------------------------------------------------- operand packing
@@ -2049,7 +2104,16 @@ namespace {
 inline int r16(int64_t x) { return (int)((x + 15) / 16 * 16); }
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr int kMaxParts = 256;
+constexpr int kMaxParts = 592;    // Gram partials: up to 4 waves of 148 CTAs (gram_waves)
+
+// CTAs per SM-slot of the Gram (DELIMIT_GRAM_WAVES, read per call): each CTA accumulates its share of the voxel
+// tiles in fp32 TMEM and writes one partial, so more waves mean shorter fp32 accumulation runs (the partials
+// are summed in float64 by gram_reduce_k).
+int gram_waves() {
+  const char* e = getenv("DELIMIT_GRAM_WAVES");
+  const int v = e ? atoi(e) : 1;
+  return v < 1 ? 1 : v > 4 ? 4 : v;
+}
 
 long long* g_prof = nullptr;   // debug: phase timestamps of the next chain3 forward launch
 
@@ -2374,12 +2438,11 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
       h2.bias2 = bias3;
       h2.rstate = rstate;
       h2.redo = 0;
-      const int slot = what[6] == 'f' ? 0 : 1;   // "chain_fwd" / "chain_bwd"
-      DL_TRY(ktimer_record(slot, 0, st));
+      h2.kt = ktrace();
+      h2.kt_slot = what[6] == 'f' ? 0 : 1;   // "chain_fwd" / "chain_bwd"
       if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
       else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));
       else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
-      DL_TRY(ktimer_record(slot, 1, st));
       v.rstate = rstate;
       v.redo = 1;
       v.prof = nullptr;
@@ -2782,7 +2845,9 @@ int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* d
       DL_REQUIRE(mid_map(&g.tm[0], g_mid, nbatch, GR, mid_pitch(nvox)) &&
                      mid_map(&g.tm[1], c_mid, nbatch, GC, mid_pitch(nvox)),
                  "chain_bwd: c_mid / g_mid must be 16-byte aligned buffers of dl_chain_mid_bytes()");
-      nparts = grid_for(gtiles, sm < kMaxParts ? sm : kMaxParts);
+      const int cap = sm * gram_waves();
+      nparts = grid_for(gtiles, cap < kMaxParts ? cap : kMaxParts);
+      g.kt = ktrace();
       DL_TRY(run_gram(g, nparts, st));
     }
     double* G = gram_out ? gram_out : reinterpret_cast<double*>(ws + w.G);

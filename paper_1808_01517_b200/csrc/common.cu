@@ -12,11 +12,9 @@ thread_local int g_launches = 0;
 std::atomic<int64_t> g_total_launches{0};
 int g_sm_count[64] = {0};   // per device ordinal, 0 = unknown
 int g_supported[64] = {0};  // 1 ok, -1 unsupported, 0 unknown
-// kernel timer (dl_ktimer_*): per slot a ring of (begin, end) event pairs, one pair per bracketed launch
-constexpr int kKtRing = 64;
+// kernel timer (dl_ktimer_*): one device trace buffer per device ordinal, allocated on the first arm
 bool g_kt_armed = false;
-cudaEvent_t g_kt_ev[2][kKtRing][2] = {};
-int64_t g_kt_n[2] = {0, 0};   // launches bracketed per slot (the ring holds the last kKtRing)
+dl::KTrace* g_kt_buf[64] = {};
 }  // namespace
 
 namespace dl {
@@ -68,17 +66,14 @@ int device_check(int* sm_count) {
   return DL_OK;
 }
 
-int ktimer_record(int slot, int end, cudaStream_t st) {
-  if (!g_kt_armed || slot < 0 || slot > 1) return DL_OK;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  DL_CUDA(cudaStreamIsCapturing(st, &cs));
-  cudaEvent_t ev = g_kt_ev[slot][g_kt_n[slot] % kKtRing][end];
-  if (cs == cudaStreamCaptureStatusActive)   // an external event node: every graph replay re-records it
-    DL_CUDA(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
-  else
-    DL_CUDA(cudaEventRecord(ev, st));
-  if (end) ++g_kt_n[slot];
-  return DL_OK;
+KTrace* ktrace() {
+  if (!g_kt_armed) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return g_kt_buf[dev];
 }
 
 }  // namespace dl
@@ -86,23 +81,50 @@ int ktimer_record(int slot, int end, cudaStream_t st) {
 extern "C" {
 
 int dl_ktimer_arm(int on) {
-  if (on && !g_kt_ev[0][0][0])
-    for (auto& ring : g_kt_ev)
-      for (auto& pair : ring)
-        for (auto& ev : pair) DL_CUDA(cudaEventCreate(&ev));
+  if (on) {
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    DL_REQUIRE(dev >= 0 && dev < 64, "ktimer_arm: device ordinal %d out of range", dev);
+    if (!g_kt_buf[dev]) {
+      dl::KTrace h{};
+      for (int s = 0; s < dl::kKtSlots; ++s) h.t[s][0][0] = ~0ull;
+      DL_CUDA(cudaMalloc(&g_kt_buf[dev], sizeof(dl::KTrace)));
+      DL_CUDA(cudaMemcpy(g_kt_buf[dev], &h, sizeof h, cudaMemcpyHostToDevice));
+    }
+  }
   g_kt_armed = on != 0;
   return DL_OK;
 }
 
-int64_t dl_ktimer_count(int slot) { return slot == 0 || slot == 1 ? g_kt_n[slot] : -1; }
+namespace {
+int ktimer_snapshot(dl::KTrace* h) {
+  int dev = 0;
+  DL_CUDA(cudaGetDevice(&dev));
+  DL_REQUIRE(dev >= 0 && dev < 64 && g_kt_buf[dev], "ktimer: never armed on device %d", dev);
+  DL_CUDA(cudaDeviceSynchronize());
+  DL_CUDA(cudaMemcpy(h, g_kt_buf[dev], sizeof *h, cudaMemcpyDeviceToHost));
+  return DL_OK;
+}
+}  // namespace
+
+int64_t dl_ktimer_count(int slot) {
+  if (slot < 0 || slot >= dl::kKtSlots) return -1;
+  dl::KTrace h;
+  if (ktimer_snapshot(&h) != DL_OK) return -1;
+  return (int64_t)h.seq[slot];
+}
 
 int dl_ktimer_read(int slot, int back, float* ms) {
-  DL_REQUIRE(slot == 0 || slot == 1, "ktimer_read: slot %d (0 forward, 1 adjoint)", slot);
-  DL_REQUIRE(ms && g_kt_ev[0][0][0], "ktimer_read: timer never armed or null output");
-  DL_REQUIRE(back >= 0 && back < kKtRing && back < g_kt_n[slot],
-             "ktimer_read: launch %d back of %lld bracketed (ring of %d)", back, (long long)g_kt_n[slot], kKtRing);
-  const auto& pair = g_kt_ev[slot][(g_kt_n[slot] - 1 - back) % kKtRing];
-  DL_CUDA(cudaEventElapsedTime(ms, pair[0], pair[1]));
+  DL_REQUIRE(slot >= 0 && slot < dl::kKtSlots, "ktimer_read: slot %d (0 forward, 1 adjoint, 2 Gram)", slot);
+  DL_REQUIRE(ms, "ktimer_read: null output");
+  dl::KTrace h;
+  DL_TRY(ktimer_snapshot(&h));
+  const int64_t n = (int64_t)h.seq[slot];
+  DL_REQUIRE(back >= 0 && back < dl::kKtRing - 1 && back < n,
+             "ktimer_read: launch %d back of %lld recorded (ring of %d)", back, (long long)n, dl::kKtRing);
+  const auto& e = h.t[slot][(n - 1 - back) % dl::kKtRing];
+  DL_REQUIRE(e[1] >= e[0] && e[0] != ~0ull, "ktimer_read: incomplete record");
+  *ms = (float)((double)(e[1] - e[0]) * 1e-6);
   return DL_OK;
 }
 

@@ -119,12 +119,13 @@ template <typename T>
 __global__ void __launch_bounds__(256) ingest_x_k(const void* __restrict__ raw, Geo g, double slope, double inter,
                                                   const int64_t* __restrict__ sel, int n_sel,
                                                   const double* __restrict__ mean, const double* __restrict__ eps,
-                                                  float* __restrict__ out, uint8_t* __restrict__ excluded) {
+                                                  float* __restrict__ out, uint8_t* __restrict__ excluded, int64_t zoff) {
   __shared__ T tile[2][kT][kT + 1];      // raw values in their stored type, double-buffered
   __shared__ double mt[2][kT][kT + 1];   // b0 means / reciprocals of the tile, [z][x] as read
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int x0 = blockIdx.x * kT, z0 = blockIdx.y * kT;
-  const int64_t y = blockIdx.z % g.Y, k0 = (blockIdx.z / g.Y) * kKB;
+  const int64_t bz = (int64_t)blockIdx.z + zoff;   // launched in grid.z chunks of <= 65535
+  const int64_t y = bz % g.Y, k0 = (bz / g.Y) * kKB;
   const int64_t nvox = g.X * g.Y * g.Z;
   const double e = *eps;
   const int X = (int)g.X, Z = (int)g.Z, sz = (int)g.sz;   // the host checks X*Y*Z < 2^31
@@ -196,11 +197,12 @@ template <typename T>
 __global__ void __launch_bounds__(256) ingest_k(const void* __restrict__ raw, Geo g, double slope, double inter,
                                                 const int64_t* __restrict__ sel, int n_sel,
                                                 const double* __restrict__ mean, const double* __restrict__ eps,
-                                                float* __restrict__ out, int xfast) {
+                                                float* __restrict__ out, int xfast, int64_t zoff) {
   __shared__ double tile[kT][kT + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t a0 = (int64_t)blockIdx.x * kT, z0 = (int64_t)blockIdx.y * kT;
-  const int64_t y = blockIdx.z % g.Y, w = blockIdx.z / g.Y;   // w = k (xfast) or x (otherwise)
+  const int64_t bz = (int64_t)blockIdx.z + zoff;   // launched in grid.z chunks of <= 65535
+  const int64_t y = bz % g.Y, w = bz / g.Y;   // w = k (xfast) or x (otherwise)
   const int64_t A = xfast ? g.X : n_sel;
   const int64_t nvox = g.X * g.Y * g.Z;
   // load: thread tx walks a (the stored-fast axis), rows j = z
@@ -227,6 +229,8 @@ __global__ void __launch_bounds__(256) ingest_k(const void* __restrict__ raw, Ge
   }
 }
 
+constexpr int64_t kMaxGridZ = 65535;
+
 template <typename T>
 int launch_all(const void* raw, const Geo& g, double slope, double inter, const int64_t* b0, int n_b0,
                const int64_t* sel, int n_sel, float* out, uint8_t* excluded, double* mean, double* part,
@@ -238,15 +242,22 @@ int launch_all(const void* raw, const Geo& g, double slope, double inter, const 
   b0_eps_k<<<1, 32, 0, st>>>(part, nb, nvox, eps);
   DL_TRY(after_launch("b0_eps_k"));
   if (n_sel > 0 && g.sx == 1) {
-    const dim3 grid((unsigned)ceil_div<int64_t>(g.X, kT), (unsigned)ceil_div<int64_t>(g.Z, kT),
-                    (unsigned)(g.Y * ceil_div<int64_t>(n_sel, kKB)));
-    ingest_x_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, excluded);
-    DL_TRY(after_launch("ingest_x_k"));
+    const int64_t nz = g.Y * ceil_div<int64_t>(n_sel, kKB);
+    for (int64_t z0 = 0; z0 < nz; z0 += kMaxGridZ) {   // grid.z is capped at 65535
+      const dim3 grid((unsigned)ceil_div<int64_t>(g.X, kT), (unsigned)ceil_div<int64_t>(g.Z, kT),
+                      (unsigned)(nz - z0 < kMaxGridZ ? nz - z0 : kMaxGridZ));
+      ingest_x_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, excluded, z0);
+      DL_TRY(after_launch("ingest_x_k"));
+    }
     if (excluded) return DL_OK;   // written by ingest_x_k
   } else if (n_sel > 0) {
-    const dim3 grid((unsigned)ceil_div<int64_t>(n_sel, kT), (unsigned)ceil_div<int64_t>(g.Z, kT), (unsigned)(g.Y * g.X));
-    ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, 0);
-    DL_TRY(after_launch("ingest_k"));
+    const int64_t nz = g.Y * g.X;
+    for (int64_t z0 = 0; z0 < nz; z0 += kMaxGridZ) {   // grid.z is capped at 65535 (e.g. 256 x 256 in-memory volumes)
+      const dim3 grid((unsigned)ceil_div<int64_t>(n_sel, kT), (unsigned)ceil_div<int64_t>(g.Z, kT),
+                      (unsigned)(nz - z0 < kMaxGridZ ? nz - z0 : kMaxGridZ));
+      ingest_k<T><<<grid, dim3(kT, 8), 0, st>>>(raw, g, slope, inter, sel, n_sel, mean, eps, out, 0, z0);
+      DL_TRY(after_launch("ingest_k"));
+    }
   }
   if (excluded) {
     const int mb = (int)(ceil_div<int64_t>(nvox, 256) < 4096 ? ceil_div<int64_t>(nvox, 256) : 4096);

@@ -24,6 +24,25 @@ def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def slab_range(x: torch.Tensor, rank: int, world: int) -> tuple[int, int]:
+    """[lo, hi) of the first spatial axis (X) that `rank` owns when one 5-D volume is split into X-slabs."""
+    if x.dim() != 5:
+        raise ValueError(f"expected a 5-D (subjects, channels, X, Y, Z) volume, got {tuple(x.shape)}")
+    return shard_range(int(x.shape[2]), rank, world)
+
+
+def voxel_slab(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    """This rank's contiguous X-slab of a 5-D volume (single-volume sharding).
+
+    The layers are per-voxel maps with no spatial coupling (fitting.py:223, lsc.py:194), so a slab is a
+    complete, independent input: its outputs are the volume's outputs on those voxels, and the LSC
+    parameter gradient of the volume is the sum of the slabs' gradients (allreduce_gradients).  This
+    replaces the reference's in-process voxel spans (lsc.py:202-220, fitting.py:169-187) with ranks.
+    """
+    lo, hi = slab_range(x, rank, world)
+    return x[:, :, lo:hi].contiguous()
+
+
 def grads_of(params: Iterable[torch.nn.Parameter]) -> list[torch.Tensor]:
     out = []
     for p in params:

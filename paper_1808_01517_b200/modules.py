@@ -6,6 +6,7 @@
                             kernel_sizes, lb_lambda=0.006, angular_distance=pi/5)
   with .sconv.weight (shells_out, shells_in, 1, K) and .sconv.bias (shells_out,)
 * SphericalChain(s2sh, lsc, sh2s): the three fused into one forward and one backward pass.
+* RoundTrip(s2sh, sh2s): Signal2SH -> SH2Signal fused (the coefficients never reach HBM).
 
 Tensors are 5-D subjects x (shells*gradients) x H x W x D, fp32 CUDA.
 Operators are built once per gradient table on the host in float64 (geometry.py)
@@ -230,7 +231,13 @@ class SphericalChain(nn.Module):
         self._state = {}   # device -> (forward, adjoint) delayed-scaling state of the fp16 chain pass
 
     def range_state(self, device):
-        """The (forward, adjoint) scale-history tensors of the fused kernels on `device` (ops.chain_state)."""
+        """The (forward, adjoint) scale-history tensors of the fused kernels on `device` (ops.chain_state).
+
+        The kernels read and update this state in place, so one module instance must not run on two streams
+        at once: concurrent calls would share the range record, and one call's in-range record could hide the
+        other's out-of-range fp16 pass.  Use one instance per concurrent stream.  (The state is deliberately
+        not keyed by stream: CUDA-graph capture runs on a side stream, and a state created inside the capture
+        would be re-zeroed by every replay.)"""
         key = str(device)
         if key not in self._state:
             self._state[key] = (ops.chain_state(device), ops.chain_state(device))
@@ -306,3 +313,51 @@ class SphericalChain(nn.Module):
         return ops.ChainFunction.apply(x, w3, None if b is None else b.float().contiguous(),
                                        self.s2sh.fit_matrix, self.s2sh.per_shell, self.lsc.fold, self.lsc.beta,
                                        self.sh2s.basis, sf, sb)
+
+
+class RoundTrip(nn.Module):
+    """Signal2SH -> SH2Signal as ONE fused op (forward + backward): y[s] = B' M_s x[s].
+
+    Equivalent to sh2s(s2sh(x)) -- signal_to_sh then sh_to_signal (fitting.py:206-250), the round trip of the
+    reference's acceptance criterion 1 -- run through the fused chain kernels with the identity in place of
+    the LSC operator, so the SH coefficients stay in tensor memory.  Channel counts outside the fused plan run
+    the two layers one after the other.
+    """
+
+    def __init__(self, s2sh: Signal2SH, sh2s: SH2Signal):
+        super().__init__()
+        if s2sh.sh_order != sh2s.sh_order:
+            raise ShapeError(f"Signal2SH order {s2sh.sh_order} does not match SH2Signal order {sh2s.sh_order}")
+        self.s2sh, self.sh2s = s2sh, sh2s
+        self._eye = {}
+        self._state = {}
+        self._fused = {}
+
+    def range_state(self, device):
+        """(forward, adjoint) delayed-scaling state of the fused kernels on `device` (single-stream use, as
+        SphericalChain.range_state)."""
+        key = str(device)
+        if key not in self._state:
+            self._state[key] = (ops.chain_state(device), ops.chain_state(device))
+        return self._state[key]
+
+    def fused(self, shells: int) -> bool:
+        if shells not in self._fused:
+            r = self.s2sh.n_coeffs
+            self._fused[shells] = ops.chain_supported(shells, shells, self.s2sh.n_gradients, r, r,
+                                                      self.sh2s.n_gradients, self.s2sh.per_shell)
+        return self._fused[shells]
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        _check_5d(x, "signal")
+        s = self.s2sh.n_shells(x.shape[1])
+        x = ops.as_device_f32(x, "signal")
+        if not self.fused(s):
+            return self.sh2s(self.s2sh(x))
+        n = s * self.s2sh.n_coeffs
+        key = (str(x.device), n)
+        if key not in self._eye:
+            self._eye[key] = torch.eye(n, dtype=torch.float32, device=x.device)
+        sf, sb = self.range_state(x.device)
+        return ops.RoundTripFunction.apply(x, self.s2sh.fit_matrix, self.s2sh.per_shell, self.sh2s.basis,
+                                           self._eye[key], sf, sb)

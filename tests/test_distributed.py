@@ -93,3 +93,51 @@ def test_sharded_backward_allreduce_equals_full_batch():
         assert slowest == float(WORLD)                        # max over ranks
         np.testing.assert_allclose(dW, dW_full, rtol=1e-12, atol=1e-12)
         np.testing.assert_allclose(db, db_full, rtol=1e-12, atol=1e-12)
+
+
+def test_voxel_slabs_partition_the_volume():
+    from paper_1808_01517_b200.distributed import slab_range, voxel_slab
+
+    x = torch.arange(2 * 3 * 7 * 2 * 2, dtype=torch.float32).view(2, 3, 7, 2, 2)
+    for world in (1, 2, 3, 4, 8):
+        slabs = [voxel_slab(x, r, world) for r in range(world)]
+        assert all(s.is_contiguous() for s in slabs)
+        assert torch.equal(torch.cat(slabs, dim=2), x)
+        assert [slab_range(x, r, world) for r in range(world)] == [shard_range(7, r, world) for r in range(world)]
+    with pytest.raises(ValueError):
+        slab_range(x[0], 0, 2)
+
+
+def _slab_worker(rank, port_no, out):
+    """One X-slab of ONE volume per rank: local backward on the slab, then the bucketed all_reduce."""
+    from paper_1808_01517_b200.distributed import voxel_slab
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        x, dy, M, geo, w, Bt = _problem()
+        xs = voxel_slab(torch.from_numpy(x[:1]), rank, WORLD).numpy()
+        dys = voxel_slab(torch.from_numpy(dy[:1]), rank, WORLD).numpy()
+        _, dW, db = port.chain_backward(xs, dys, M, geo, w, Bt, 2)
+        weight = torch.nn.Parameter(torch.zeros(w.shape, dtype=torch.float64))
+        bias = torch.nn.Parameter(torch.zeros(2, dtype=torch.float64))
+        weight.grad = torch.from_numpy(np.ascontiguousarray(dW))
+        bias.grad = torch.from_numpy(np.ascontiguousarray(db))
+        allreduce_gradients([weight, bias])
+        out[rank] = (xs.shape[2], weight.grad.numpy().copy(), bias.grad.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_voxel_slab_backward_allreduce_equals_full_volume():
+    """Single-volume sharding: per-slab gradients summed over ranks == the volume's gradient."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_slab_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    x, dy, M, geo, w, Bt = _problem()
+    _, dW_full, db_full = port.chain_backward(x[:1], dy[:1], M, geo, w, Bt, 2)
+    assert sorted(out[r][0] for r in range(WORLD)) == [1, 2]
+    for r in range(WORLD):
+        np.testing.assert_allclose(out[r][1], dW_full, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(out[r][2], db_full, rtol=1e-12, atol=1e-12)

@@ -98,3 +98,27 @@ def test_ingest_feeds_the_chain(dev, exp):
     s2sh = dl.Signal2SH(4, tables, lb_lambda=0.006).to(dev)
     c = s2sh(vol.data)
     assert c.shape == (1, 2 * 15, 9, 7, 6) and torch.isfinite(c).all()
+
+
+def test_in_memory_256x256_grid_z_chunks(dev):
+    """A C-contiguous (X, Y, Z, V) array with X * Y = 65536 > 65535 (the CUDA grid.z cap): ingest_k walks the
+    (x, y) plane in grid.z chunks.  Also the x-fastest path with Y * ceil(n_sel / 48) > 65535."""
+    rng = np.random.default_rng(9)
+    X, Y, Z = 256, 256, 4
+    bvals = [0.0, 1000.0, 1000.0, 2000.0, 2000.0, 0.0]
+    raw = rng.uniform(50.0, 150.0, size=(X, Y, Z, len(bvals))).astype(np.float32)
+    vol, mask = dl.normalize_b0(raw, bvals, device=dev)
+    f = raw.astype(np.float64)
+    b0 = (f[..., 0] + f[..., 5]) / 2.0
+    ref = np.moveaxis(f[..., [1, 2, 3, 4]] / b0[..., None], 3, 0)[None]
+    close_fp32(vol.data, ref)
+    assert not mask.any()
+    # x-fastest (Fortran) layout with many y rows: grid.z = Y * ceil(n_sel / 48) = 70000 * 1
+    X2, Y2, Z2 = 2, 70000, 1
+    raw2 = rng.uniform(50.0, 150.0, size=(X2, Y2, Z2, len(bvals))).astype(np.float32)
+    t2 = torch.from_numpy(np.asfortranarray(raw2))
+    assert t2.stride()[0] == 1
+    vol2, _ = dl.normalize_b0(t2, bvals, device=dev)
+    f2 = raw2.astype(np.float64)
+    b02 = (f2[..., 0] + f2[..., 5]) / 2.0
+    close_fp32(vol2.data, np.moveaxis(f2[..., [1, 2, 3, 4]] / b02[..., None], 3, 0)[None])
