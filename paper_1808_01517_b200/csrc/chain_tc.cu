@@ -510,6 +510,7 @@ struct Chain3 {
   int redo;                           // chain3v bf16 pass: check the fp16 pass's ranges, recompute if needed
   dl::KTrace* kt;                     // kernel timer (dl_ktimer_*) or null, and its slot
   int kt_slot;
+  uint32_t sm_tring;                  // chain2h fused MSE: per-OUT-warp target rings (2 x 16 x 32 fp32), or 0
 };
 
 // Delayed scaling of the fp16 chain (state words, caller-owned, zero-initialised):
@@ -1321,11 +1322,28 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #define DL_OB2H 1
 #endif
 constexpr int kOB2h = DL_OB2H;   // D3 chunks an OUT warp loads before releasing / storing them
+// A2 released item by item as the last output shell's stage-2 MMAs read it (a2_ifree), so CONV converts the
+// next tile's items while that shell's MMAs still run; 0: one a2_free for the whole tile (measurement knob)
+#ifndef DL_A2_ITEM
+#define DL_A2_ITEM 1
+#endif
+constexpr bool kA2Item = DL_A2_ITEM != 0;
+// CONV writes an item's Gram term planes after handing the item to the stage-2 MMA (1) or before (0)
+#ifndef DL_MID_LATE
+#define DL_MID_LATE 1
+#endif
+constexpr bool kMidLate = DL_MID_LATE != 0;
+// CONV loads all its items of a stage-1 group, then releases the D1 buffer before converting them (1)
+#ifndef DL_D1_EARLY
+#define DL_D1_EARLY 0
+#endif
+constexpr bool kD1Early = DL_D1_EARLY != 0;
 struct Bars2h {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t d1g_full[2], d1g_free[2];
   uint64_t a2_full[16], a2_free;
+  uint64_t a2_ifree[16];                            // item k of A2 read by the last output shell's MMAs
   uint64_t d3_full[2], d3_free[2];
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
   uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
@@ -1384,6 +1402,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     }
     for (int k = 0; k < nk2; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting item k
     mbar_init(&bars.a2_free, 1);
+    for (int k = 0; k < 16; ++k) mbar_init(&bars.a2_ifree[k], 1);
     for (int c = 0; c < p.NAc; ++c) {
       mbar_init(&bars.c_full[c], 4);
       mbar_init(&bars.c_empty[c], 1);
@@ -1441,13 +1460,68 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       uint16_t* mid = (p.mid && vx < p.mid_pitch)
                           ? p.mid + ((b * (p.mid_pitch >> 6) + (vx >> 6)) * 2 * K2) * 64 + (vx & 63)
                           : nullptr;
-      if (!KOUT && it > 0) {   // the previous tile's stage-2 MMAs have read A2
+      if (!KOUT && !kA2Item && it > 0) {   // the previous tile's stage-2 MMAs have read A2
         role_wait(&bars.a2_free, (it - 1) & 1);
       }
+      // one D1 item -> its A2 slot (+ the Gram term planes)
+      auto conv_item = [&](int i, float (&v)[16]) {
+        track16<H>(v, amax);
+        uint32_t w[PARTS][8];
+        split16<PARTS, H>(v, w);
+        if (kA2Item && it > 0) {
+          role_wait(&bars.a2_ifree[i], (it - 1) & 1);
+          fence_after();
+        }
+        store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
+        tmem_wait_st();
+        fence_before();
+        warp_arrive(&bars.a2_full[i]);
+        if (mid) {
+          float u[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
+          uint32_t m[2][8];
+          split16<2>(u, m);
+          store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
+        }
+      };
       for (int g = 0; g < p.G1; ++g, ++gq) {
         const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
         role_wait(&bars.d1g_full[buf], (gq / nb) & 1);
         fence_after();
+        if (kD1Early && !KOUT && kMidLate && n1c <= 2 * kCVQ) {
+          // load this warp's (at most two) items of the group, release D1 to the stage-1 MMA at once, then convert
+          uint32_t ra[16], rb[16];
+          int ia = -1, ib = -1;
+          for (int c = 0; c < n1c; ++c) {
+            const int i = g * n1c + c;
+            if (i % kCVQ != cw) continue;
+            const uint32_t a = tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16;
+            if (ia < 0) {
+              ia = i;
+              tmem_ld<16>(a, ra);
+            } else {
+              ib = i;
+              tmem_ld<16>(a, rb);
+            }
+          }
+          tmem_wait_ld();
+          fence_before();
+          warp_arrive(&bars.d1g_free[buf]);
+          if (ia >= 0) {
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(ra[e]);
+            conv_item(ia, v);
+          }
+          if (ib >= 0) {
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(rb[e]);
+            conv_item(ib, v);
+          }
+          continue;
+        }
         for (int c = 0; c < n1c; ++c) {
           const int i = g * n1c + c;
           if (i % kCVQ != cw) continue;   // the CONV warps of a quadrant take items round-robin
@@ -1456,7 +1530,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           track16<H>(v, amax);
           uint32_t w[PARTS][8];
           split16<PARTS, H>(v, w);
-          if (mid) {
+          if (mid && !kMidLate) {
             float u[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
@@ -1474,10 +1548,22 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             fence_before();
             warp_arrive(&bars.c_full[slot]);
           } else {
+            if (kA2Item && it > 0) {   // the previous tile's last-shell MMA has read item i
+              role_wait(&bars.a2_ifree[i], (it - 1) & 1);
+              fence_after();
+            }
             store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
             tmem_wait_st();
             fence_before();
             warp_arrive(&bars.a2_full[i]);
+          }
+          if (mid && kMidLate) {   // the Gram term planes after the A2 handoff: off the MMA's critical path
+            float u[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
+            uint32_t m[2][8];
+            split16<2>(u, m);
+            store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
           }
         }
         fence_before();
@@ -1495,6 +1581,54 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     const int nck = p.N3 / 16;
     uint32_t n3 = 0;
     double lacc = 0.0;
+    // Fused MSE with a target ring (kOB2h == 1): this warp's target chunks (16 channels x its 32 voxels) are
+    // copied one chunk ahead by per-thread cp.async into a private 2-stage ring, so the loads overlap the
+    // previous chunk's arithmetic and stores instead of stalling them (each thread reads back only what it
+    // copied: cp.async.wait_group is the only synchronisation).  Safe when target aliases out: a chunk's
+    // target elements are read before that chunk's outputs are written, and chunks never overlap.
+    const bool tring = p.target && p.sm_tring && kOB2h == 1 && !KOUT;
+    float* tr = reinterpret_cast<float*>(smem + p.sm_tring) + ow * 1024;
+    int64_t nt_t = blockIdx.x;   // next target chunk to issue: tile, shell, chunk
+    int nt_o = 0, nt_ck = cg;
+    uint32_t tq_issue = 0, tq_use = 0;
+    // 8-byte copies (two voxels per lane, two rows per instruction) when every row start is 8-byte aligned
+    const bool t8 = (p.nvox % 2 == 0) && ((uintptr_t)p.target % 8 == 0) && (p.out_bs % 2 == 0);
+    auto t_issue = [&]() {
+      __syncwarp();   // every lane has read the stage this copy overwrites (lanes read each other's copies)
+      if (nt_t < ntiles) {
+        const int64_t bb_ = nt_t / p.tiles_per_b;
+        if (t8) {
+          const int64_t v0q = (nt_t - bb_ * p.tiles_per_b) * kTileV + 32 * qd;
+          const int nrow = p.C3 - nt_ck * 16, pv = 2 * (lane & 15);
+          const int64_t vv = v0q + pv;
+          const uint32_t nb = vv + 1 < p.nvox ? 8u : vv < p.nvox ? 4u : 0u;
+          const float* src = p.target + bb_ * p.out_bs + ((int64_t)nt_o * p.C3 + nt_ck * 16) * stride + (nb ? vv : 0);
+          float* dst = tr + (tq_issue & 1) * 512 + pv;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 2 * i + (lane >> 4);
+            const bool ok = r < nrow && nb;
+            cp_async8(dst + r * 32, ok ? src + (int64_t)r * stride : p.target, ok ? nb : 0u);
+          }
+        } else {
+          const int64_t vv = (nt_t - bb_ * p.tiles_per_b) * kTileV + row;
+          const bool ok = vv < p.nvox;
+          const float* src = p.target + bb_ * p.out_bs + ((int64_t)nt_o * p.C3 + nt_ck * 16) * stride + (ok ? vv : 0);
+          stream_chunk(tr + (tq_issue & 1) * 512 + lane, src, stride, ok ? p.C3 - nt_ck * 16 : 0, p.target);
+        }
+        nt_ck += kOUTQ;
+        if (nt_ck >= nck) {
+          nt_ck = cg;
+          if (++nt_o == p.G2) {
+            nt_o = 0;
+            nt_t += gridDim.x;
+          }
+        }
+      }
+      cp_async_commit();
+      ++tq_issue;
+    };
+    if (tring) t_issue();
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t b = t / p.tiles_per_b, v = (t - b * p.tiles_per_b) * kTileV + row;
       const bool vok = v < p.nvox;
@@ -1504,7 +1638,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       }
       for (int o = 0; o < p.G2; ++o, ++n3) {
         const uint32_t xb = KOUT ? 0u : (n3 & 1);
-        if (p.target && vok) {   // fused MSE: pull this shell's target rows into L2 while the MMA runs
+        if (p.target && vok && !tring) {   // fused MSE: pull this shell's target rows into L2 while the MMA runs
           for (int ck = cg; ck < nck; ck += kOUTQ) {
             const int nval = p.C3 - ck * 16;
             const float* tg = p.target + b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
@@ -1531,12 +1665,34 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
 #pragma unroll
           for (int k = 0; k < kOB2h; ++k) {
             const int ck = c0 + k * kOUTQ;
-            if (ck >= nck || !vok || !p.out) continue;
+            if (tring && ck < nck) {   // this chunk's target is in ring stage tq_use & 1; start the next copy
+              t_issue();
+              cp_async_wait<1>();
+              __syncwarp();   // the 8-byte path reads values other lanes copied
+            }
+            if (ck >= nck || !vok || !p.out) {
+              if (tring && ck < nck) ++tq_use;
+              continue;
+            }
             const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
             float* d = p.out + off;
             const int nval = p.C3 - ck * 16;
             const float* bb = sb + o * p.N3 + ck * 16;
-            if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
+            if (tring) {   // fused MSE from the target ring: d(loss)/dy and the squared residuals
+              const float* tv = tr + (tq_use & 1) * 512 + lane;
+              ++tq_use;
+              float csum = 0.f;   // 16 squares in fp32, then one float64 add per chunk
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                if (nval >= 16 || e < nval) {
+                  const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - tv[e * 32];
+                  csum = fmaf(res, res, csum);
+                  __stcs(d, res * p.out_scale);
+                }
+                d += stride;
+              }
+              lacc += (double)csum;
+            } else if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
               // all 16 target loads first: the stores below could alias them, so loads interleaved with
               // stores would each wait out a full memory latency
               const float* tg = p.target + off;
@@ -1569,6 +1725,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
         }
       }
     }
+    if (tring) cp_async_wait<0>();
     if (p.target) loss_publish(p.loss, lacc);
   } else if (warp == kW3MMA || warp == kW3MMA2) {
     // =========================== MMA issuers ===========================
@@ -1692,7 +1849,10 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
               mbar_wait_warp(&bars.a2_full[k], it & 1);
               fence_after();
             }
-            if (elect_one()) kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == 0);
+            if (elect_one()) {
+              kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == 0);
+              if (kA2Item && o == p.G2 - 1) commit(&bars.a2_ifree[k]);   // CONV may overwrite item k
+            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < PARTS; ++j) bd[j] += ks2;
@@ -1700,7 +1860,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           if (elect_one()) {
             commit(&bars.d3_full[xb]);
             if (p.tstream) commit(&bars.t_empty[xb]);
-            if (o == p.G2 - 1) commit(&bars.a2_free);
+            if (!kA2Item && o == p.G2 - 1) commit(&bars.a2_free);
           }
           __syncwarp();
 #pragma unroll
@@ -2343,6 +2503,11 @@ bool plan_chain2h(Chain3& p, bool kout) {
   p.tstream = (!kout && !resident && tbufs < (size_t)parts * p.w2_img) ? 1 : 0;
   p.sm_w2 = (uint32_t)o; o = al(o + (p.tstream ? tbufs : (size_t)parts * p.w2_img), 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N3 * 4, 128);
+  p.sm_tring = 0;
+  if (p.target && !kout && kOB2h == 1 && !getenv("DELIMIT_NO_TRING")) {   // fused MSE target rings
+    p.sm_tring = (uint32_t)o;
+    o = al(o + (size_t)kOUT3 * 2 * 16 * 32 * 4, 128);
+  }
   p.sm_ring = (uint32_t)o;
   for (int ns : {12, 8, 4}) {
     p.ns = ns;

@@ -178,14 +178,30 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+// DL_WAIT_HINT_NS > 0: every mbarrier wait passes a suspend-time hint, so a waiting warp is parked by the
+// hardware until the phase completes instead of re-issuing try_wait / yield / branch (measured: without it the
+// polling loops are ~35% of chain2h's issued instructions in an issue-bound kernel).
+#ifndef DL_WAIT_HINT_NS
+#define DL_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  if (DL_WAIT_HINT_NS > 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(DL_WAIT_HINT_NS)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+  }
 }
 
 // Whole-warp wait with a suspend-time hint: the hardware may park the warp until the phase completes
@@ -262,6 +278,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0,
 // 4-byte asynchronous global -> shared copy (LDGSTS); src_bytes = 0 zero-fills the destination.
 __device__ __forceinline__ void cp_async4(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+// 8-byte asynchronous global -> shared copy; src_bytes in {0, 4, 8} (the rest zero-filled).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
