@@ -1333,11 +1333,6 @@ constexpr bool kA2Item = DL_A2_ITEM != 0;
 #define DL_MID_LATE 1
 #endif
 constexpr bool kMidLate = DL_MID_LATE != 0;
-// CONV loads all its items of a stage-1 group, then releases the D1 buffer before converting them (1)
-#ifndef DL_D1_EARLY
-#define DL_D1_EARLY 0
-#endif
-constexpr bool kD1Early = DL_D1_EARLY != 0;
 struct Bars2h {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
@@ -1463,65 +1458,10 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       if (!KOUT && !kA2Item && it > 0) {   // the previous tile's stage-2 MMAs have read A2
         role_wait(&bars.a2_free, (it - 1) & 1);
       }
-      // one D1 item -> its A2 slot (+ the Gram term planes)
-      auto conv_item = [&](int i, float (&v)[16]) {
-        track16<H>(v, amax);
-        uint32_t w[PARTS][8];
-        split16<PARTS, H>(v, w);
-        if (kA2Item && it > 0) {
-          role_wait(&bars.a2_ifree[i], (it - 1) & 1);
-          fence_after();
-        }
-        store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
-        tmem_wait_st();
-        fence_before();
-        warp_arrive(&bars.a2_full[i]);
-        if (mid) {
-          float u[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
-          uint32_t m[2][8];
-          split16<2>(u, m);
-          store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
-        }
-      };
       for (int g = 0; g < p.G1; ++g, ++gq) {
         const uint32_t nb = p.G1 >= 2 ? 2u : 1u, buf = gq % nb;
         role_wait(&bars.d1g_full[buf], (gq / nb) & 1);
         fence_after();
-        if (kD1Early && !KOUT && kMidLate && n1c <= 2 * kCVQ) {
-          // load this warp's (at most two) items of the group, release D1 to the stage-1 MMA at once, then convert
-          uint32_t ra[16], rb[16];
-          int ia = -1, ib = -1;
-          for (int c = 0; c < n1c; ++c) {
-            const int i = g * n1c + c;
-            if (i % kCVQ != cw) continue;
-            const uint32_t a = tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16;
-            if (ia < 0) {
-              ia = i;
-              tmem_ld<16>(a, ra);
-            } else {
-              ib = i;
-              tmem_ld<16>(a, rb);
-            }
-          }
-          tmem_wait_ld();
-          fence_before();
-          warp_arrive(&bars.d1g_free[buf]);
-          if (ia >= 0) {
-            float v[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(ra[e]);
-            conv_item(ia, v);
-          }
-          if (ib >= 0) {
-            float v[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(rb[e]);
-            conv_item(ib, v);
-          }
-          continue;
-        }
         for (int c = 0; c < n1c; ++c) {
           const int i = g * n1c + c;
           if (i % kCVQ != cw) continue;   // the CONV warps of a quadrant take items round-robin

@@ -128,7 +128,7 @@ int dl_ktimer_read(int slot, int back, float* ms) {
   return DL_OK;
 }
 
-int dl_abi_version(void) { return 104; }
+int dl_abi_version(void) { return 105; }
 
 const char* dl_last_error(void) { return g_err; }
 

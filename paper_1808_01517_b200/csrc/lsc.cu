@@ -33,11 +33,13 @@ __global__ void build_operator_k(const float* __restrict__ P, const float* __res
 
 // ---- Gram partials: partial[p][row][col] = sum over this CTA's voxel tiles of g[row] * c_aug[col]
 // where c_aug = [c; 1] (the ones column yields sum_v g for the bias gradient).
-constexpr int kGT = 144;     // output tile edge (16 thread groups x 9)
-constexpr int kGPer = 9;     // rows / cols per thread
+// Output tile edge GT = 16 thread groups x GPER rows / cols per thread: 144 (9 x 9 per thread) for 3-shell
+// operators, 48 (3 x 3) when rows and cols + 1 fit one 48 tile (a single-shell order-8 LSC: 45 x 46), so a
+// small Gram does not pay for a 144 x 144 tile.
 constexpr int kGVK = 32;     // voxels per shared-memory stage
 constexpr int kMaxParts = 512;
 
+template <int kGT, int kGPer>
 __global__ void __launch_bounds__(256, 2)
 gram_k(const float* __restrict__ g, const float* __restrict__ c, float* __restrict__ partials, int rows,
        int cols, int64_t nvox, int64_t g_bs, int64_t c_bs, int64_t nbatch, int64_t tiles_per_b) {
@@ -94,13 +96,33 @@ gram_k(const float* __restrict__ g, const float* __restrict__ c, float* __restri
   }
 }
 
-// Fixed-order float64 sum of the partials.
-__global__ void reduce_parts_k(const float* __restrict__ partials, double* __restrict__ G, int nparts,
-                               int64_t n) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += (double)__ldg(partials + (int64_t)p * n + e);
-    G[e] = s;
+// Fixed-order float64 sum of the partials.  Block (32, 8): lane x takes one element, row y a contiguous chunk
+// of parts (loads of eight parts in flight); the chunk sums are added in chunk order (deterministic).
+__global__ void __launch_bounds__(256) reduce_parts_k(const float* __restrict__ partials, double* __restrict__ G,
+                                                      int nparts, int64_t n) {
+  __shared__ double red[8][33];
+  const int64_t e = blockIdx.x * 32LL + threadIdx.x;
+  const int per = (nparts + 7) / 8;
+  const int q0 = threadIdx.y * per, q1 = q0 + per < nparts ? q0 + per : nparts;
+  double s = 0.0;
+  if (e < n) {
+    int q = q0;
+    for (; q + 8 <= q1; q += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(partials + (int64_t)(q + j) * n + e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += (double)v[j];
+    }
+    for (; q < q1; ++q) s += (double)__ldg(partials + (int64_t)q * n + e);
+  }
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && e < n) {
+    double t = red[0][threadIdx.x];
+#pragma unroll
+    for (int c = 1; c < 8; ++c) t += red[c][threadIdx.x];
+    G[e] = t;
   }
 }
 
@@ -173,20 +195,26 @@ int lsc_wgrad(const float* g, const float* c, const float* P, const float* beta,
       (reinterpret_cast<uintptr_t>(partials + (int64_t)kMaxParts * n) + 255) & ~uintptr_t(255));
   const int64_t tiles_per_b = ceil_div<int64_t>(nvox, kGVK);
   const int64_t ntiles = nbatch * tiles_per_b;
-  const int rt = ceil_div(rows, kGT), ct = ceil_div(cols + 1, kGT);
+  const bool small = rows <= 48 && cols + 1 <= 48;
+  const int gt = small ? 48 : 144;
+  const int rt = ceil_div(rows, gt), ct = ceil_div(cols + 1, gt);
   int64_t parts = (int64_t)sm * 2 / (rt * ct);
   if (parts < 1) parts = 1;
   if (parts > kMaxParts) parts = kMaxParts;
   if (parts > ntiles) parts = ntiles > 0 ? ntiles : 1;
   if (ntiles > 0) {
     DL_REQUIRE(g && c, "lsc_wgrad: null g/c");
-    gram_k<<<dim3((unsigned)parts, rt, ct), 256, 0, st>>>(g, c, partials, rows, cols, nvox, g_bs, c_bs,
-                                                         nbatch, tiles_per_b);
+    if (small)
+      gram_k<48, 3><<<dim3((unsigned)parts, rt, ct), 256, 0, st>>>(g, c, partials, rows, cols, nvox, g_bs, c_bs,
+                                                                  nbatch, tiles_per_b);
+    else
+      gram_k<144, 9><<<dim3((unsigned)parts, rt, ct), 256, 0, st>>>(g, c, partials, rows, cols, nvox, g_bs, c_bs,
+                                                                   nbatch, tiles_per_b);
     DL_TRY(after_launch("lsc_gram"));
   } else {
     DL_CUDA(cudaMemsetAsync(partials, 0, n * sizeof(float), st));
   }
-  reduce_parts_k<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, G, (int)parts, n);
+  reduce_parts_k<<<(unsigned)((n + 31) / 32), dim3(32, 8), 0, st>>>(partials, G, (int)parts, n);
   DL_TRY(after_launch("lsc_reduce_parts"));
   finalize_k<<<(unsigned)(s_out * s_in * K + s_out), 256, 0, st>>>(G, P, beta, dW, db, (int)s_out, (int)s_in,
                                                                    (int)K, (int)r_out, (int)r_in);

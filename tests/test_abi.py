@@ -57,7 +57,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_workspace_queries(lib):
-    assert lib.dl_abi_version() == 104
+    assert lib.dl_abi_version() == 105
     n = (3 * 45) * (3 * 45 + 1)
     assert lib.dl_lsc_wgrad_workspace_bytes(3, 3, 45, 45) >= n * 8
     ws = lib.dl_chain_workspace_bytes(1, 3, 3, 90, 45, 45, 90, 1000)
