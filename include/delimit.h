@@ -122,6 +122,23 @@ size_t dl_chain_mid_bytes(int64_t nbatch, int64_t shells, int64_t r, int64_t nvo
 size_t dl_chain_workspace_bytes(int64_t nbatch, int64_t s_in, int64_t s_out, int64_t n, int64_t r_in,
                                 int64_t r_out, int64_t n_out, int64_t nvox);
 size_t dl_chain_state_bytes(void);
+/* The fused Signal2SH -> LSC -> SH2Signal forward read straight from a raw acquisition: the b0 normalisation of
+ * fitting.normalize_b0 (fitting.py:253-342) runs in the kernel's input role, x[c][v] = raw[sel[c]][v] * vox_a[v] +
+ * vox_b[v], so the normalised volume never exists in memory.  raw: the acquisition's
+ * volumes, `vstride` elements apart (even), int16 (raw_dtype 4) or float32 (16), voxels in stored order; sel
+ * (device int32, s_in * n): the stored volume of every chain input channel (shell-blocked); vox_a / vox_b from
+ * dl_b0_voxel_scale_f32.  y: (s_out * n_out, nvox) fp32 in the same stored voxel order.  3-term bf16 pass. */
+int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const int* sel, const float* vox_a,
+                         const float* vox_b, float* y, const float* M, int m_per_shell, const float* L,
+                         const float* bvec, const float* Bt, void* workspace, int64_t s_in, int64_t s_out, int64_t n,
+                         int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+/* Per-voxel factors of the raw-input chain from the b0 volumes (fitting.py:253-342 in float64, rounded once):
+ * vox_a = slope / mean_b0, vox_b = inter / mean_b0 (slope 0: no scaling), 0 where mean_b0 <= 1e-6 max(mean_b0);
+ * excluded (optional) the mask; all in stored voxel order.  Needs the x-fastest NIfTI layout (sx = 1, sy = X,
+ * sz = X Y); workspace: dl_normalize_b0_workspace_bytes(X, Y, Z). */
+int dl_b0_voxel_scale_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, int64_t Z, int64_t sx, int64_t sy,
+                          int64_t sz, int64_t sv, double slope, double inter, const int64_t* b0_idx, int64_t n_b0,
+                          float* vox_a, float* vox_b, uint8_t* excluded, void* workspace, void* stream);
 /*
  * Forward fused with a mean-squared-error loss against `target` (same layout as y): writes
  * dy = 2 (y - target) / numel(y) instead of y, and loss[2] = mean((y - target)^2) (loss: 4 doubles of

@@ -55,7 +55,7 @@ from .functional import (
 )
 
 from . import dwio
-from .ingest import load_dwi, normalize_b0
+from .ingest import chain_from_raw, load_dwi, normalize_b0
 
 __version__ = "0.1.0"
 

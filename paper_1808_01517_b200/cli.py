@@ -195,19 +195,26 @@ def cmd_lsc(a) -> int:
 
 
 def cmd_chain(a) -> int:
+    """normalize_b0 -> signal2sh -> lsc -> sh2signal of one acquisition.  The b0 normalisation runs inside the fused
+    chain kernel, which reads the file's stored volumes (ingest.chain_from_raw); the output comes back in the
+    file's voxel order, which is also the order the output NIfTI stores."""
     from . import modules as M
 
-    vol, _, scheme = ingest.load_dwi(a.dwi, a.bvals, a.bvecs, shells=a.shell)
-    tables = np.stack([scheme.shell_directions(b) for b in scheme.shell_bvalues()])
-    kernel, sizes, alpha = _kernel_from_args(a, vol.shells)
+    raw = dwio.read_nifti_raw(a.dwi)
+    scheme = dwio.read_bvals_bvecs(a.bvals, a.bvecs)
+    if len(raw.shape) != 4:
+        raise ShapeError(f"raw acquisition must be 4-D, got shape {raw.shape}")
+    _, table = ingest.select_volumes(scheme, int(raw.shape[3]), shells=a.shell)
+    sub = ingest._sub_scheme(scheme, table, scheme.b0_threshold)
+    tables = np.stack([sub.shell_directions(b) for b in sub.shell_bvalues()])
+    kernel, sizes, alpha = _kernel_from_args(a, len(table))
     s2sh = M.Signal2SH(a.order, tables, lb_lambda=a.lb_lambda).cuda()
     lsc = M.LocalSphericalConvolution(kernel.shells_in, kernel.shells_out, a.order, a.order, tables[0], sizes,
                                       lb_lambda=a.lb_lambda, angular_distance=alpha).cuda()
     lsc.load_kernel(kernel)
     sh2s = M.SH2Signal(a.order, tables[0]).cuda()
-    with torch.no_grad():
-        y = M.SphericalChain(s2sh, lsc, sh2s)(vol.data)
-    _to_nifti(y, a.out, dwio.read_nifti_raw(a.dwi).affine)
+    y, _, _ = ingest.chain_from_raw(M.SphericalChain(s2sh, lsc, sh2s), raw, scheme, shells=a.shell)
+    _to_nifti(y, a.out, raw.affine)
     return 0
 
 

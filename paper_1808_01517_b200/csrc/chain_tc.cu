@@ -321,6 +321,80 @@ __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, in
   if (H) *amax = fmaxf(*amax, am);
 }
 
+// IN role over a RAW acquisition (b0 normalisation folded into the chain's input):
+// channel c of the chain input is stored volume sel[c] of the acquisition (volumes `vstride` elements apart,
+// voxels in the acquisition's stored order), in its stored type T (int16 or fp32), and
+//   x[c][v] = raw[sel[c]][v] * vox_a[v] + vox_b[v]
+// with vox_a = slope / mean_b0, vox_b = inter / mean_b0 (0 for excluded voxels) -- fitting.normalize_b0
+// (fitting.py:253-342) applied on the fly, so the normalised volume never exists in HBM.  One warp per lane
+// quadrant; each warp streams its 32 voxels of every chunk through a private NS-deep shared-memory ring with
+// cp.async (two voxels per lane, two rows per instruction: 16 rows x 32 voxels per stage), NS - 1 chunks ahead.
+// Needs an even vstride and T-aligned rows (checked on the host).
+template <int PARTS, int NS, typename T, typename Geo>
+__device__ __forceinline__ void in_role_raw(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
+                                            int64_t nvox, const T* raw, int64_t vstride, const int* sel,
+                                            const float* vox_a, const float* vox_b, uint32_t tslots, int NA,
+                                            uint64_t* a_full, uint64_t* a_empty, T* ring) {
+  constexpr int kV = 2 * (int)sizeof(T);   // bytes per lane per copy (two voxels)
+  const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31, pv = 2 * (lane & 15), half = lane >> 4;
+  const int64_t nmine = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * per_tile;
+  int64_t qp = 0;
+  uint32_t pslot = 0, cslot = 0, aslot = 0, around = 0;
+  auto issue = [&]() {
+    __syncwarp();   // every lane has read the stage this copy refills (lanes read each other's copies)
+    if (qp < total) {
+      const int64_t ti = qp / per_tile;
+      const int r = (int)(qp - ti * per_tile);
+      const int64_t t = blockIdx.x + ti * gridDim.x, b = t / tiles_per_b;
+      const int64_t v = (t - b * tiles_per_b) * kTileV + 32 * qd + pv;
+      const ChunkGeo cg = geo(r);
+      const int nval = cg.nval < 16 ? cg.nval : 16;
+      const int vsel = lane < nval ? __ldg(sel + cg.c0 + lane) : 0;   // lane j < 16 holds row j's volume
+      const uint32_t nb = v + 1 < nvox ? (uint32_t)kV : v < nvox ? (uint32_t)sizeof(T) : 0u;
+      T* dst = ring + pslot * 512 + pv;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = 2 * i + half;
+        const int vol = __shfl_sync(0xffffffffu, vsel, row);
+        const bool ok = row < nval && nb;
+        const T* src = ok ? raw + (int64_t)vol * vstride + v : raw;
+        if constexpr (kV == 8) cp_async8(dst + row * 32, src, ok ? nb : 0u);
+        else cp_async4(dst + row * 32, src, ok ? nb : 0u);
+      }
+      ++qp;
+    }
+    cp_async_commit();
+    pslot = pslot + 1 == NS ? 0 : pslot + 1;
+  };
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) issue();
+  int64_t cur_t = -1;
+  float a = 0.f, bb = 0.f;
+  for (int64_t q = 0; q < total; ++q) {
+    issue();
+    cp_async_wait<NS - 1>();
+    __syncwarp();   // the stage holds every lane's copies
+    const int64_t ti = q / per_tile;
+    const int r = (int)(q - ti * per_tile);
+    if (ti != cur_t) {   // this thread's voxel scale for the tile
+      cur_t = ti;
+      const int64_t t = blockIdx.x + ti * gridDim.x, b = t / tiles_per_b;
+      const int64_t v = (t - b * tiles_per_b) * kTileV + 32 * qd + lane;
+      a = v < nvox ? __ldg(vox_a + b * nvox + v) : 0.f;
+      bb = v < nvox ? __ldg(vox_b + b * nvox + v) : 0.f;
+    }
+    const int nval = geo(r).nval;
+    const T* rp = ring + cslot * 512 + lane;
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = j < nval ? fmaf((float)rp[j * 32], a, bb) : 0.f;
+    cslot = cslot + 1 == NS ? 0 : cslot + 1;
+    put_a<PARTS, false>(x, tslots, NA, a_full, a_empty, aslot, around, 1);
+  }
+  cp_async_wait<0>();
+}
+
 // TMA loader (one warp, one elected lane issues): chunk (tile, r) -> ring stage, as two 8 x 132 boxes of
 // the channel-pair view (even channels first, then odd).  A box must start 16-byte aligned in global
 // memory; odd channel rows start at voxel offset nvox, so when nvox % 4 == 2 their box starts 2 voxels
@@ -511,6 +585,12 @@ struct Chain3 {
   dl::KTrace* kt;                     // kernel timer (dl_ktimer_*) or null, and its slot
   int kt_slot;
   uint32_t sm_tring;                  // chain2h fused MSE: per-OUT-warp target rings (2 x 16 x 32 fp32), or 0
+  const void* raw;                    // chain3v raw-acquisition input (in_role_raw) or null
+  int raw_type;                       // NIfTI datatype code of raw: 4 int16, 16 float32
+  int64_t raw_vstride;                // elements between stored volumes
+  const int* raw_sel;                 // stored volume of each chain input channel (device)
+  const float* vox_a;                 // per-voxel slope / mean_b0 and inter / mean_b0 (stored order)
+  const float* vox_b;
 };
 
 // Delayed scaling of the fp16 chain (state words, caller-owned, zero-initialised):
@@ -984,7 +1064,20 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
   if (warp < kIN3) {
     // =========================== IN ===========================
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
-    if (p.tma && p.cpi == 2) {
+    if (p.raw) {
+      if constexpr (!H) {
+        if (warp < 4 && p.raw_type == 4)
+          in_role_raw<PARTS, NS, int16_t>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox,
+                                          reinterpret_cast<const int16_t*>(p.raw), p.raw_vstride, p.raw_sel, p.vox_a,
+                                          p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+                                          reinterpret_cast<int16_t*>(smem + p.sm_ring) + warp * NS * 512);
+        else if (warp < 4)
+          in_role_raw<PARTS, NS, float>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox,
+                                        reinterpret_cast<const float*>(p.raw), p.raw_vstride, p.raw_sel, p.vox_a,
+                                        p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+                                        reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
+      }
+    } else if (p.tma && p.cpi == 2) {
       if constexpr (NS % 4 == 0)
         in_role_tma2<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
                                                   bars.a_full, bars.a_empty,
@@ -2868,6 +2961,51 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
   dl::begin_call();
   return dl::tc::chain_fwd(x, y, c_mid, M, m_per_shell, L, bvec, Bt, workspace, state, nbatch, s_in, s_out, n, r_in,
                            r_out, n_out, nvox, stream, nullptr, 0.f, nullptr);
+}
+
+// The fused chain read straight from a raw acquisition (b0 normalisation in the IN role, in_role_raw): the
+// 3-term bf16 pass, forward only; y is (s_out * n_out, nvox) in the acquisition's stored voxel order.
+int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const int* sel, const float* vox_a,
+                         const float* vox_b, float* y, const float* M, int m_per_shell, const float* L,
+                         const float* bvec, const float* Bt, void* workspace, int64_t s_in, int64_t s_out, int64_t n,
+                         int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+  using namespace dl::tc;
+  dl::begin_call();
+  int sm = 0;
+  DL_TRY(dl::device_check(&sm));
+  DL_REQUIRE(raw && sel && vox_a && vox_b && y && M && L && Bt && workspace, "chain_fwd_raw: null pointer");
+  DL_REQUIRE(raw_dtype == 4 || raw_dtype == 16, "chain_fwd_raw: raw datatype %d (int16 = 4, float32 = 16 only)",
+             raw_dtype);
+  const int esz = raw_dtype == 4 ? 2 : 4;
+  DL_REQUIRE(vstride % 2 == 0 && vstride >= nvox && (uintptr_t)raw % (2 * esz) == 0,
+             "chain_fwd_raw: volumes must start on %d-byte boundaries (even stride, aligned base)", 2 * esz);
+  DL_REQUIRE(nvox >= 0 && s_in >= 1 && s_out >= 1 && n >= 1 && r_in >= 1 && r_out >= 1 && n_out >= 1,
+             "chain_fwd_raw: bad sizes");
+  Dims d = make_dims(1, s_in, s_out, n, r_in, r_out, n_out, nvox, m_per_shell);
+  d.parts = 3;
+  DL_REQUIRE(chain_fits(d), "chain_fwd_raw: channel counts exceed the fused kernel's TMEM/smem plan");
+  if (nvox == 0) return DL_OK;
+  WsLayout w = ws_layout(d, kMaxParts);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  cudaStream_t st = dl::as_stream(stream);
+  DL_TRY(pack_all(d, w, ws, M, L, Bt, false, st));
+  Chain3 p = chain3_params(d, w, ws, false);
+  p.in = nullptr;
+  p.out = y;
+  p.mid = nullptr;
+  p.mid_pitch = mid_pitch(nvox);
+  p.mid_ones = -1;
+  p.bias2 = bvec;
+  p.tma = 0;
+  p.raw = raw;
+  p.raw_type = raw_dtype;
+  p.raw_vstride = vstride;
+  p.raw_sel = sel;
+  p.vox_a = vox_a;
+  p.vox_b = vox_b;
+  Chain3 v = p;
+  DL_REQUIRE(use_v3() && plan_chain3v(v, 3), "chain_fwd_raw: needs the chain3v plan");
+  return run_chain3v<3>(v, grid_for(p.tiles_per_b, sm), st);
 }
 
 int dl_chain_fwd_mse_f32(const float* x, const float* target, float* dy, void* c_mid, const float* M, int m_per_shell,

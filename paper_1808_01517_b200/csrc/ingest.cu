@@ -107,6 +107,22 @@ __global__ void mask_k(Geo g, const double* __restrict__ mean, const double* __r
   }
 }
 
+// Per-voxel normalisation factors for the chain's raw-input path (in_role_raw), in stored (walk) order:
+// x = raw * a + b with a = slope / mean_b0, b = inter / mean_b0 (slope 0: no scaling, a = 1 / mean_b0, b = 0),
+// both 0 for excluded voxels (mean_b0 <= eps); excluded (optional) in walk order.
+__global__ void voxel_scale_k(int64_t nvox, const double* __restrict__ mean, const double* __restrict__ eps,
+                              double slope, double inter, float* __restrict__ a, float* __restrict__ b,
+                              uint8_t* __restrict__ excluded) {
+  const double e = *eps;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x) {
+    const double mu = mean[i];
+    const bool ex = mu <= e;
+    a[i] = ex ? 0.f : (float)((slope != 0.0 ? slope : 1.0) / mu);
+    b[i] = ex ? 0.f : (float)((slope != 0.0 ? inter : 0.0) / mu);
+    if (excluded) excluded[i] = ex ? 1 : 0;
+  }
+}
+
 // x-fastest stored layout (a NIfTI file's bytes): tile over (x, z) for one y and kKB consecutive output
 // channels; the tile's float64 b0 means are staged in shared memory once and reused for every channel.
 // Grid: (ceil(X / 32), ceil(Z / 32), Y * ceil(n_sel / kKB)); block 32 x 8.
@@ -267,10 +283,53 @@ int launch_all(const void* raw, const Geo& g, double slope, double inter, const 
   return DL_OK;
 }
 
+template <typename T>
+int launch_scale(const void* raw, const Geo& g, double slope, double inter, const int64_t* b0, int n_b0, float* va,
+                 float* vb, uint8_t* excluded, double* mean, double* part, double* eps, cudaStream_t st) {
+  const int64_t nvox = g.X * g.Y * g.Z;
+  const int nb = (int)(ceil_div<int64_t>(nvox, 256) < kMeanBlocks ? ceil_div<int64_t>(nvox, 256) : kMeanBlocks);
+  b0_mean_k<T><<<nb, 256, 0, st>>>(raw, g, slope, inter, b0, n_b0, mean, part);
+  DL_TRY(after_launch("b0_mean_k"));
+  b0_eps_k<<<1, 32, 0, st>>>(part, nb, nvox, eps);
+  DL_TRY(after_launch("b0_eps_k"));
+  const int mb = (int)(ceil_div<int64_t>(nvox, 256) < 4096 ? ceil_div<int64_t>(nvox, 256) : 4096);
+  voxel_scale_k<<<mb, 256, 0, st>>>(nvox, mean, eps, slope, inter, va, vb, excluded);
+  return after_launch("voxel_scale_k");
+}
+
 }  // namespace
 }  // namespace dl
 
 extern "C" {
+
+int dl_b0_voxel_scale_f32(const void* raw, int nifti_dtype, int64_t X, int64_t Y, int64_t Z, int64_t sx, int64_t sy,
+                          int64_t sz, int64_t sv, double slope, double inter, const int64_t* b0_idx, int64_t n_b0,
+                          float* vox_a, float* vox_b, uint8_t* excluded, void* workspace, void* stream) {
+  using namespace dl;
+  begin_call();
+  DL_TRY(device_check(nullptr));
+  DL_REQUIRE(X >= 1 && Y >= 1 && Z >= 1 && n_b0 >= 1 && n_b0 < (1 << 30) && X * Y * Z < 2147483647LL,
+             "b0_voxel_scale: bad sizes (X %lld, Y %lld, Z %lld, b0 %lld)", (long long)X, (long long)Y, (long long)Z,
+             (long long)n_b0);
+  DL_REQUIRE(raw && b0_idx && vox_a && vox_b && workspace, "b0_voxel_scale: null pointer");
+  DL_REQUIRE(sx == 1 && sy == X && sz == X * Y, "b0_voxel_scale: needs the x-fastest dense volume layout (NIfTI)");
+  Geo g;
+  g.X = X; g.Y = Y; g.Z = Z; g.sx = sx; g.sy = sy; g.sz = sz; g.sv = sv;
+  g.d0 = 0; g.d1 = 1; g.d2 = 2; g.e0 = X; g.e1 = Y;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  double* mean = reinterpret_cast<double*>(ws);
+  double* part = mean + 2 * X * Y * Z;
+  double* eps = part + kMeanBlocks;
+  cudaStream_t st = as_stream(stream);
+  switch (nifti_dtype) {
+    case 2: return launch_scale<uint8_t>(raw, g, slope, inter, b0_idx, (int)n_b0, vox_a, vox_b, excluded, mean, part, eps, st);
+    case 4: return launch_scale<int16_t>(raw, g, slope, inter, b0_idx, (int)n_b0, vox_a, vox_b, excluded, mean, part, eps, st);
+    case 8: return launch_scale<int32_t>(raw, g, slope, inter, b0_idx, (int)n_b0, vox_a, vox_b, excluded, mean, part, eps, st);
+    case 16: return launch_scale<float>(raw, g, slope, inter, b0_idx, (int)n_b0, vox_a, vox_b, excluded, mean, part, eps, st);
+    case 64: return launch_scale<double>(raw, g, slope, inter, b0_idx, (int)n_b0, vox_a, vox_b, excluded, mean, part, eps, st);
+    default: return fail(DL_EINVAL, "b0_voxel_scale: unsupported NIfTI datatype code %d", nifti_dtype);
+  }
+}
 
 size_t dl_normalize_b0_workspace_bytes(int64_t X, int64_t Y, int64_t Z) {
   const int64_t nvox = X * Y * Z;

@@ -9,6 +9,12 @@ the b0 mean, scaling, division and the move to channel-major order cost one pass
 
 load_dwi(nifti, bvals, bvecs, ...) goes from files to the hot path's input: the voxel bytes are read once
 (dwio.read_nifti_raw), staged in pinned memory, copied to the device as stored and normalised there.
+
+chain_from_raw(chain, raw, bvals_or_scheme, ...) fuses the normalisation INTO the chain:
+the fused Signal2SH -> LSC -> SH2Signal kernel reads the acquisition's stored volumes (int16 / float32, x fastest)
+and applies x = raw * slope / mean_b0 in its input role (dl_chain_fwd_raw_f32), so the normalised volume never
+exists; the output comes back in the acquisition's voxel order as a (1, C, X, Y, Z) view -- exactly the layout a
+NIfTI file of the result stores.
 """
 
 from __future__ import annotations
@@ -122,3 +128,84 @@ def load_dwi(nifti_path: str, bvals_path: str, bvecs_path: str, shells: Sequence
     scheme = dwio.read_bvals_bvecs(bvals_path, bvecs_path, b0_threshold=b0_threshold, tolerance=tolerance)
     vol, mask = normalize_b0(dwio.read_nifti_raw(nifti_path), scheme, b0_threshold, tolerance, shells, device)
     return vol, mask, vol.scheme
+
+
+def _stage_raw(raw, dev):
+    """(device tensor of the stored elements, NIfTI code, (X, Y, Z, V), strides, slope, inter)."""
+    slope, inter = 0.0, 0.0
+    if isinstance(raw, dwio.NiftiRaw):
+        if len(raw.shape) != 4:
+            raise ShapeError(f"raw acquisition must be 4-D, got shape {raw.shape}")
+        if raw.scaled:
+            slope, inter = raw.slope, raw.inter
+        src = np.ascontiguousarray(raw.data)
+        host = torch.empty(src.shape, dtype=_TORCH_OF[src.dtype.type], pin_memory=torch.cuda.is_available())
+        host.numpy()[...] = src
+        return host.to(dev, non_blocking=True), raw.dtype_code, tuple(raw.shape), raw.strides(), slope, inter
+    t = raw if isinstance(raw, torch.Tensor) else torch.from_numpy(np.asarray(raw))
+    if t.dim() != 4:
+        raise ShapeError(f"raw acquisition must be 4-D, got shape {tuple(t.shape)}")
+    if t.dtype not in _CODE_OF_TORCH:
+        t = t.to(torch.float64)
+    t = t.to(dev)
+    return t, _CODE_OF_TORCH[t.dtype], tuple(t.shape), t.stride(), slope, inter
+
+
+def chain_from_raw(chain, raw, bvals_or_scheme, b0_threshold: float = dwio.B0_THRESHOLD,
+                   tolerance: float = dwio.SHELL_TOLERANCE, shells: Sequence[float] | None = None, device=None):
+    """chain(normalize_b0(raw)) in one pass over the acquisition (fitting.py:253-342 then the chain).
+
+    chain: a SphericalChain whose Signal2SH matches the selected shells (its per-shell or shared tables are the
+    caller's; channel c = shell s, direction i reads stored volume shell[s].indices[i]).  raw: dwio.NiftiRaw or an
+    (X, Y, Z, V) array / tensor.  Returns (y, excluded, sub-scheme): y the chain output as a (1, C, X, Y, Z)
+    float32 CUDA tensor, excluded the (X, Y, Z) bool mask.  When the acquisition is int16 / float32 in the
+    x-fastest layout with volumes contiguous (a NIfTI file's bytes) and the chain fits the fused plan, the
+    normalisation runs inside the chain kernel (dl_chain_fwd_raw_f32) and y is a view in the stored voxel order;
+    otherwise normalize_b0 then chain (two passes, y C-contiguous).  Forward only (no autograd).
+    """
+    from . import ops
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t, code, shape4, strides, slope, inter = _stage_raw(raw, dev)
+    X, Y, Z, V = (int(e) for e in shape4)
+    b0_idx, table = select_volumes(bvals_or_scheme, V, b0_threshold, tolerance, shells)
+    scheme = bvals_or_scheme if isinstance(bvals_or_scheme, dwio.GradientScheme) else None
+    sub = _sub_scheme(scheme, table, b0_threshold)
+    sel = np.concatenate([s_.indices for s_ in table]).astype(np.int64)
+    layers = chain._layers
+    first, last = layers[0], layers[-1]
+    s_in, n = len(table), int(table[0].indices.size)
+    nvox = X * Y * Z
+    fused = (code in (4, 16) and tuple(int(a) for a in strides) == (1, X, X * Y, nvox) and nvox % 2 == 0
+             and s_in == first.shells_in and n == chain.s2sh.n_gradients and chain.fused())
+    if not fused:
+        vol, mask = normalize_b0(raw, bvals_or_scheme, b0_threshold, tolerance, shells, dev)
+        with torch.no_grad():
+            return chain(vol.data), mask, sub
+    lib = _lib.load()
+    b0_t = torch.as_tensor(b0_idx, dtype=torch.int64).to(dev)
+    va = torch.empty(nvox, dtype=torch.float32, device=dev)
+    vb = torch.empty(nvox, dtype=torch.float32, device=dev)
+    ex = torch.empty(nvox, dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(lib.dl_normalize_b0_workspace_bytes(X, Y, Z)), dtype=torch.uint8, device=dev)
+    sx, sy, sz, sv = (int(a) for a in strides)
+    _lib.call("dl_b0_voxel_scale_f32", _p(t), int(code), X, Y, Z, sx, sy, sz, sv, ctypes.c_double(slope),
+              ctypes.c_double(inter), _p(b0_t), len(b0_idx), _p(va), _p(vb), _p(ex), _p(ws), _stream())
+    with torch.no_grad():
+        args = []
+        for layer in layers:
+            w, b = layer.sconv.weight, layer.sconv.bias
+            args.append((w.reshape(w.shape[0], w.shape[1], w.shape[3]).float().contiguous(),
+                         None if b is None else b.float().contiguous(), layer.fold, layer.beta))
+        _, _, L, bvec = ops._fold_layers(args)
+    s_out, r_in, r_out = last.shells_out, first.r_in, last.r_out
+    n_out = chain.sh2s.n_gradients
+    sel_t = torch.as_tensor(sel, dtype=torch.int32).to(dev)
+    y = torch.empty((s_out * n_out, Z, Y, X), dtype=torch.float32, device=dev)
+    wsc = torch.empty(int(lib.dl_chain_workspace_bytes(1, s_in, s_out, n, r_in, r_out, n_out, nvox)),
+                      dtype=torch.uint8, device=dev)
+    _lib.call("dl_chain_fwd_raw_f32", _p(t), int(code), sv, _p(sel_t), _p(va), _p(vb), _p(y),
+              _p(chain.s2sh.fit_matrix), int(chain.s2sh.per_shell), _p(L), _p(bvec), _p(chain.sh2s.basis), _p(wsc),
+              s_in, s_out, n, r_in, r_out, n_out, nvox, _stream())
+    mask = ex.view(Z, Y, X).permute(2, 1, 0).bool()
+    return y.permute(0, 3, 2, 1).unsqueeze(0), mask, sub

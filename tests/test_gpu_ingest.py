@@ -122,3 +122,85 @@ def test_in_memory_256x256_grid_z_chunks(dev):
     f2 = raw2.astype(np.float64)
     b02 = (f2[..., 0] + f2[..., 5]) / 2.0
     close_fp32(vol2.data, np.moveaxis(f2[..., [1, 2, 3, 4]] / b02[..., None], 3, 0)[None])
+
+
+def _chain_for(dev, tables, order=4, seed=3):
+    from paper_1808_01517_b200.directions import unit_sphere_directions  # noqa: F401
+
+    rng = np.random.default_rng(seed)
+    s = tables.shape[0]
+    s2sh = dl.Signal2SH(order, tables, lb_lambda=0.006).to(dev)
+    lsc = dl.LocalSphericalConvolution(s, s, order, order, tables[0], [5], lb_lambda=0.006,
+                                       angular_distance=np.pi / 5).to(dev)
+    lsc.load_kernel(dl.LscKernel(rng.normal(size=(s, s, 6)) / (6 * s), rng.normal(size=s) * 0.1))
+    return dl.SphericalChain(s2sh, lsc, dl.SH2Signal(order, tables[0]).to(dev)), s2sh, lsc
+
+
+def test_chain_from_raw_matches_reference(dev, exp):
+    """normalize_b0 fused into the chain kernel == the reference's normalize_b0 output
+    (expected.npz, made by sphdwi) pushed through the oracle chain, at the LSC tolerance; mask identical."""
+    from oracle import port
+
+    raw = dwio.read_nifti_raw(os.path.join(G, "acq.nii.gz"))
+    scheme = dwio.read_bvals_bvecs(os.path.join(G, "acq.bval"), os.path.join(G, "acq.bvec"))
+    sub = dl.normalize_b0(raw, scheme, device=dev)[0].scheme
+    tables = np.stack([sub.shell_directions(b) for b in sub.shell_bvalues()])
+    chain, s2sh, lsc = _chain_for(dev, tables)
+    y, mask, sub2 = dl.chain_from_raw(chain, raw, scheme, device=dev)
+    assert tuple(y.shape) == (1, 2 * 6, 9, 7, 6) and not y.is_contiguous()   # stored (x-fastest) voxel order
+    assert np.array_equal(mask.cpu().numpy(), exp["mask"]) and np.array_equal(sub2.bvals, exp["sub_bvals"])
+    Ms = [op.fit_matrix for op in s2sh.operators]
+    geo = port.lsc_geometry(tables[0], [5], np.pi / 5, 4, 4, 0.006)
+    w = lsc.sconv.weight.detach().double().cpu().numpy()[:, :, 0, :]
+    b = lsc.sconv.bias.detach().double().cpu().numpy()
+    y_ref = port.chain_forward(exp["vol"], Ms, geo, w, b, port.eval_basis(tables[0], 4), 2)
+    assert port.rel_err(y.double().cpu().numpy(), y_ref) <= 1e-4
+    # and equal to the two-pass path (normalize_b0 volume -> fused chain) at the same tolerance
+    vol, _ = dl.normalize_b0(raw, scheme, device=dev)
+    with torch.no_grad():
+        y2 = chain(vol.data)
+    assert port.rel_err(y.double().cpu().numpy(), y2.double().cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["f32_fortran", "i16_fortran_scaled", "c_order_fallback"])
+def test_chain_from_raw_layouts(dev, kind):
+    """Larger volumes (several 128-voxel tiles + a tail): float32 and scaled int16 stored x-fastest run fused; a
+    C-ordered in-memory array takes the two-pass fallback; all match normalize_b0 -> chain."""
+    from oracle import port
+
+    rng = np.random.default_rng(11)
+    X, Y, Z = 38, 21, 13                       # nvox = 10374 (even): 81 tiles + a tail of 6
+    bvals = np.array([0.0] + [1000.0] * 30 + [0.0] + [2000.0] * 30)
+    dirs = rng.normal(size=(bvals.size, 3))
+    scheme_dirs = dirs / np.linalg.norm(dirs, axis=1, keepdims=True)
+    scheme = dwio.GradientScheme(scheme_dirs, bvals, np.array([0, 31]),
+                                 (dwio.Shell(1000.0, np.arange(1, 31)), dwio.Shell(2000.0, np.arange(32, 62))),
+                                 dwio.B0_THRESHOLD)
+    stored = rng.uniform(200.0, 3000.0, size=(X, Y, Z, bvals.size))
+    stored[..., [0, 31]] += 2000.0
+    if kind == "i16_fortran_scaled":
+        arr = stored.astype(np.int16)
+        raw = dwio.NiftiRaw(np.asfortranarray(arr).ravel(order="F"), arr.shape, dwio.CODE_OF[np.dtype(np.int16)],
+                            0.5, 10.0, np.eye(4), {})
+        ref_in = arr.astype(np.float64) * 0.5 + 10.0
+    elif kind == "f32_fortran":
+        arr = stored.astype(np.float32)
+        raw = torch.from_numpy(np.asfortranarray(arr))
+        ref_in = arr.astype(np.float64)
+    else:
+        arr = stored.astype(np.float32)
+        raw = np.ascontiguousarray(arr)
+        ref_in = arr.astype(np.float64)
+    tables = np.stack([scheme_dirs[1:31], scheme_dirs[32:62]])
+    chain, s2sh, lsc = _chain_for(dev, tables)
+    y, mask, _ = dl.chain_from_raw(chain, raw, scheme, device=dev)
+    assert y.is_contiguous() == (kind == "c_order_fallback")
+    b0 = ref_in[..., [0, 31]].mean(axis=3)
+    xn = np.moveaxis(ref_in[..., list(range(1, 31)) + list(range(32, 62))] / b0[..., None], 3, 0)[None]
+    Ms = [op.fit_matrix for op in s2sh.operators]
+    geo = port.lsc_geometry(tables[0], [5], np.pi / 5, 4, 4, 0.006)
+    w = lsc.sconv.weight.detach().double().cpu().numpy()[:, :, 0, :]
+    b = lsc.sconv.bias.detach().double().cpu().numpy()
+    y_ref = port.chain_forward(xn, Ms, geo, w, b, port.eval_basis(tables[0], 4), 2)
+    assert port.rel_err(y.double().cpu().numpy(), y_ref) <= 1e-4
+    assert not mask.any()
