@@ -127,11 +127,13 @@ size_t dl_chain_state_bytes(void);
  * vox_b[v], so the normalised volume never exists in memory.  raw: the acquisition's
  * volumes, `vstride` elements apart (even), int16 (raw_dtype 4) or float32 (16), voxels in stored order; sel
  * (device int32, s_in * n): the stored volume of every chain input channel (shell-blocked); vox_a / vox_b from
- * dl_b0_voxel_scale_f32.  y: (s_out * n_out, nvox) fp32 in the same stored voxel order.  3-term bf16 pass. */
+ * dl_b0_voxel_scale_f32.  y: (s_out * n_out, nvox) fp32 in the same stored voxel order.  state: as for
+ * dl_chain_fwd_f32 (fp16 pass + bf16 check; NULL: the 3-term bf16 pass alone). */
 int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const int* sel, const float* vox_a,
                          const float* vox_b, float* y, const float* M, int m_per_shell, const float* L,
-                         const float* bvec, const float* Bt, void* workspace, int64_t s_in, int64_t s_out, int64_t n,
-                         int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream);
+                         const float* bvec, const float* Bt, void* workspace, void* state, int64_t s_in,
+                         int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox,
+                         void* stream);
 /* Per-voxel factors of the raw-input chain from the b0 volumes (fitting.py:253-342 in float64, rounded once):
  * vox_a = slope / mean_b0, vox_b = inter / mean_b0 (slope 0: no scaling), 0 where mean_b0 <= 1e-6 max(mean_b0);
  * excluded (optional) the mask; all in stored voxel order.  Needs the x-fastest NIfTI layout (sx = 1, sy = X,

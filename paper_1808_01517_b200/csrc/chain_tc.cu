@@ -330,17 +330,19 @@ __device__ __forceinline__ void in_role_cpasync(const Geo& geo, int per_tile, in
 // quadrant; each warp streams its 32 voxels of every chunk through a private NS-deep shared-memory ring with
 // cp.async (two voxels per lane, two rows per instruction: 16 rows x 32 voxels per stage), NS - 1 chunks ahead.
 // Needs an even vstride and T-aligned rows (checked on the host).
-template <int PARTS, int NS, typename T, typename Geo>
+template <int PARTS, int NS, typename T, typename Geo, bool H = false>
 __device__ __forceinline__ void in_role_raw(const Geo& geo, int per_tile, int64_t ntiles, int64_t tiles_per_b,
                                             int64_t nvox, const T* raw, int64_t vstride, const int* sel,
                                             const float* vox_a, const float* vox_b, uint32_t tslots, int NA,
-                                            uint64_t* a_full, uint64_t* a_empty, T* ring) {
+                                            uint64_t* a_full, uint64_t* a_empty, T* ring, int iw, int nIW,
+                                            float sc = 1.f, float* amax = nullptr) {
   constexpr int kV = 2 * (int)sizeof(T);   // bytes per lane per copy (two voxels)
   const int qd = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31, pv = 2 * (lane & 15), half = lane >> 4;
   const int64_t nmine = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = nmine * per_tile;
-  int64_t qp = 0;
-  uint32_t pslot = 0, cslot = 0, aslot = 0, around = 0;
+  float am = 0.f;
+  int64_t qp = iw;   // this warp's chunks: iw, iw + nIW, ...
+  uint32_t pslot = 0, cslot = 0, aslot = (uint32_t)(iw % NA), around = (uint32_t)(iw / NA);
   auto issue = [&]() {
     __syncwarp();   // every lane has read the stage this copy refills (lanes read each other's copies)
     if (qp < total) {
@@ -362,7 +364,7 @@ __device__ __forceinline__ void in_role_raw(const Geo& geo, int per_tile, int64_
         if constexpr (kV == 8) cp_async8(dst + row * 32, src, ok ? nb : 0u);
         else cp_async4(dst + row * 32, src, ok ? nb : 0u);
       }
-      ++qp;
+      qp += nIW;
     }
     cp_async_commit();
     pslot = pslot + 1 == NS ? 0 : pslot + 1;
@@ -371,13 +373,13 @@ __device__ __forceinline__ void in_role_raw(const Geo& geo, int per_tile, int64_
   for (int j = 0; j < NS - 1; ++j) issue();
   int64_t cur_t = -1;
   float a = 0.f, bb = 0.f;
-  for (int64_t q = 0; q < total; ++q) {
+  for (int64_t q = iw; q < total; q += nIW) {
     issue();
     cp_async_wait<NS - 1>();
     __syncwarp();   // the stage holds every lane's copies
     const int64_t ti = q / per_tile;
     const int r = (int)(q - ti * per_tile);
-    if (ti != cur_t) {   // this thread's voxel scale for the tile
+    if (ti != cur_t) {   // this thread's voxel factors for the tile
       cur_t = ti;
       const int64_t t = blockIdx.x + ti * gridDim.x, b = t / tiles_per_b;
       const int64_t v = (t - b * tiles_per_b) * kTileV + 32 * qd + lane;
@@ -390,9 +392,11 @@ __device__ __forceinline__ void in_role_raw(const Geo& geo, int per_tile, int64_
 #pragma unroll
     for (int j = 0; j < 16; ++j) x[j] = j < nval ? fmaf((float)rp[j * 32], a, bb) : 0.f;
     cslot = cslot + 1 == NS ? 0 : cslot + 1;
-    put_a<PARTS, false>(x, tslots, NA, a_full, a_empty, aslot, around, 1);
+    scale16<H>(x, sc, am);
+    put_a<PARTS, H>(x, tslots, NA, a_full, a_empty, aslot, around, nIW);
   }
   cp_async_wait<0>();
+  if (H) *amax = fmaxf(*amax, am);
 }
 
 // TMA loader (one warp, one elected lane issues): chunk (tile, r) -> ring stage, as two 8 x 132 boxes of
@@ -1065,18 +1069,18 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
     // =========================== IN ===========================
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
     if (p.raw) {
-      if constexpr (!H) {
-        if (warp < 4 && p.raw_type == 4)
-          in_role_raw<PARTS, NS, int16_t>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox,
-                                          reinterpret_cast<const int16_t*>(p.raw), p.raw_vstride, p.raw_sel, p.vox_a,
-                                          p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
-                                          reinterpret_cast<int16_t*>(smem + p.sm_ring) + warp * NS * 512);
-        else if (warp < 4)
-          in_role_raw<PARTS, NS, float>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox,
-                                        reinterpret_cast<const float*>(p.raw), p.raw_vstride, p.raw_sel, p.vox_a,
-                                        p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
-                                        reinterpret_cast<float*>(smem + p.sm_ring) + warp * NS * 512);
-      }
+      // all 8 IN warps (two per quadrant, alternate chunks), each with a private ring: NS stages of 1 KB (int16)
+      // or NS / 2 stages of 2 KB (fp32) -- 8 KB per ring stage slot of the plan
+      if (p.raw_type == 4)
+        in_role_raw<PARTS, NS, int16_t, decltype(geo), H>(
+            geo, per_tile, ntiles, p.tiles_per_b, p.nvox, reinterpret_cast<const int16_t*>(p.raw), p.raw_vstride,
+            p.raw_sel, p.vox_a, p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+            reinterpret_cast<int16_t*>(smem + p.sm_ring) + warp * NS * 512, warp >> 2, 2, sc, &amax);
+      else
+        in_role_raw<PARTS, NS / 2, float, decltype(geo), H>(
+            geo, per_tile, ntiles, p.tiles_per_b, p.nvox, reinterpret_cast<const float*>(p.raw), p.raw_vstride,
+            p.raw_sel, p.vox_a, p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+            reinterpret_cast<float*>(smem + p.sm_ring) + warp * (NS / 2) * 512, warp >> 2, 2, sc, &amax);
     } else if (p.tma && p.cpi == 2) {
       if constexpr (NS % 4 == 0)
         in_role_tma2<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
@@ -1516,7 +1520,18 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   if (warp < kIN3) {
     // =========================== IN (as chain3v) ===========================
     const uint32_t tslots = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + p.colA;
-    if (p.tma && p.cpi == 2) {
+    if (p.raw) {   // raw acquisition input (in_role_raw, one chunk per IN item)
+      if (p.raw_type == 4)
+        in_role_raw<PARTS, NS, int16_t, decltype(geo), H>(
+            geo, per_tile, ntiles, p.tiles_per_b, p.nvox, reinterpret_cast<const int16_t*>(p.raw), p.raw_vstride,
+            p.raw_sel, p.vox_a, p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+            reinterpret_cast<int16_t*>(smem + p.sm_ring) + warp * NS * 512, warp >> 2, 2, sc, &amax);
+      else
+        in_role_raw<PARTS, NS / 2, float, decltype(geo), H>(
+            geo, per_tile, ntiles, p.tiles_per_b, p.nvox, reinterpret_cast<const float*>(p.raw), p.raw_vstride,
+            p.raw_sel, p.vox_a, p.vox_b, tslots, p.NA, bars.a_full, bars.a_empty,
+            reinterpret_cast<float*>(smem + p.sm_ring) + warp * (NS / 2) * 512, warp >> 2, 2, sc, &amax);
+    } else if (p.tma && p.cpi == 2) {
       if constexpr (NS % 4 == 0)
         in_role_tma2<PARTS, NS, decltype(geo), H>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, tslots, p.NA,
                                                   bars.a_full, bars.a_empty,
@@ -2503,12 +2518,13 @@ bool use_2h() {
 // stage-1 image | folded T images | folded bias | TMA ring (a multiple of 4 deep) | barriers.
 bool plan_chain2h(Chain3& p, bool kout) {
   constexpr int parts = 2;
-  if (!p.tma || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2 || (kout && p.G2 > 4))
+  if ((!p.tma && !p.raw) || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2 ||
+      (kout && (p.G2 > 4 || p.raw)))
     return false;
   const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1;
   const int D3w = kout ? p.G2 * p.N3 : 2 * p.N3;
   int A2w = p.G1 * p.N1;
-  p.cpi = getenv("DELIMIT_IN_SINGLE") ? 1 : 2;   // measurement knob: one chunk per IN item
+  p.cpi = (getenv("DELIMIT_IN_SINGLE") || p.raw) ? 1 : 2;   // raw input: one chunk per item; else a measurement knob
   if (kout) {   // two IN items, the rest A2 ring slots (>= 2)
     p.NA = 2;
     p.NAc = (512 - D1w - D3w - 2 * 2 * parts * 8) / (parts * 8);
@@ -2967,8 +2983,9 @@ int dl_chain_fwd_f32(const float* x, float* y, void* c_mid, const float* M, int 
 // 3-term bf16 pass, forward only; y is (s_out * n_out, nvox) in the acquisition's stored voxel order.
 int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const int* sel, const float* vox_a,
                          const float* vox_b, float* y, const float* M, int m_per_shell, const float* L,
-                         const float* bvec, const float* Bt, void* workspace, int64_t s_in, int64_t s_out, int64_t n,
-                         int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+                         const float* bvec, const float* Bt, void* workspace, void* state, int64_t s_in,
+                         int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox,
+                         void* stream) {
   using namespace dl::tc;
   dl::begin_call();
   int sm = 0;
@@ -2982,13 +2999,13 @@ int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const 
   DL_REQUIRE(nvox >= 0 && s_in >= 1 && s_out >= 1 && n >= 1 && r_in >= 1 && r_out >= 1 && n_out >= 1,
              "chain_fwd_raw: bad sizes");
   Dims d = make_dims(1, s_in, s_out, n, r_in, r_out, n_out, nvox, m_per_shell);
-  d.parts = 3;
   DL_REQUIRE(chain_fits(d), "chain_fwd_raw: channel counts exceed the fused kernel's TMEM/smem plan");
   if (nvox == 0) return DL_OK;
   WsLayout w = ws_layout(d, kMaxParts);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   cudaStream_t st = dl::as_stream(stream);
-  DL_TRY(pack_all(d, w, ws, M, L, Bt, false, st));
+  const bool h = state && fp16_pass();
+  DL_TRY(pack_all(d, w, ws, M, L, Bt, h, st));
   Chain3 p = chain3_params(d, w, ws, false);
   p.in = nullptr;
   p.out = y;
@@ -3004,8 +3021,16 @@ int dl_chain_fwd_raw_f32(const void* raw, int raw_dtype, int64_t vstride, const 
   p.vox_a = vox_a;
   p.vox_b = vox_b;
   Chain3 v = p;
-  DL_REQUIRE(use_v3() && plan_chain3v(v, 3), "chain_fwd_raw: needs the chain3v plan");
-  return run_chain3v<3>(v, grid_for(p.tiles_per_b, sm), st);
+  DL_REQUIRE(use_v3() && plan_chain3v(v, d.parts), "chain_fwd_raw: needs the chain3v plan");
+  // with a state: the fp16 pass (chain2h with SH2Signal folded into T, else chain3v; delayed scaling) and the bf16
+  // check pass, all reading the raw volumes
+  const bool fold = h && use_2h();
+  if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, bvec, false, st));
+  return run_chain(p, d, grid_for(p.tiles_per_b, sm), st, "chain_fwd", h ? reinterpret_cast<uint32_t*>(state) : nullptr,
+                   reinterpret_cast<const uint16_t*>(ws + w.imgMh), reinterpret_cast<const uint16_t*>(ws + w.imgLh),
+                   reinterpret_cast<const uint16_t*>(ws + w.imgBh),
+                   fold ? reinterpret_cast<const uint16_t*>(ws + w.imgTh) : nullptr,
+                   reinterpret_cast<const float*>(ws + w.b3));
 }
 
 int dl_chain_fwd_mse_f32(const float* x, const float* target, float* dy, void* c_mid, const float* M, int m_per_shell,

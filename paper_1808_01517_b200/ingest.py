@@ -204,8 +204,9 @@ def chain_from_raw(chain, raw, bvals_or_scheme, b0_threshold: float = dwio.B0_TH
     y = torch.empty((s_out * n_out, Z, Y, X), dtype=torch.float32, device=dev)
     wsc = torch.empty(int(lib.dl_chain_workspace_bytes(1, s_in, s_out, n, r_in, r_out, n_out, nvox)),
                       dtype=torch.uint8, device=dev)
+    sf, _ = chain.range_state(dev)   # the fp16 pass's scale history (the same signal distribution as chain(x))
     _lib.call("dl_chain_fwd_raw_f32", _p(t), int(code), sv, _p(sel_t), _p(va), _p(vb), _p(y),
               _p(chain.s2sh.fit_matrix), int(chain.s2sh.per_shell), _p(L), _p(bvec), _p(chain.sh2s.basis), _p(wsc),
-              s_in, s_out, n, r_in, r_out, n_out, nvox, _stream())
+              _p(sf), s_in, s_out, n, r_in, r_out, n_out, nvox, _stream())
     mask = ex.view(Z, Y, X).permute(2, 1, 0).bool()
     return y.permute(0, 3, 2, 1).unsqueeze(0), mask, sub
