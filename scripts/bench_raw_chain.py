@@ -6,7 +6,7 @@ warm-ups):
   two-pass   ingest.normalize_b0 (fp32 (1, 270, X, Y, Z) volume in HBM) -> SphericalChain forward (fp16 pass)
   fused      ingest.chain_from_raw: b0 factors (dl_b0_voxel_scale_f32) + the chain kernel reading the int16
              volumes with the normalisation in its input role (dl_chain_fwd_raw_f32, 3-term bf16 pass)
-and checks the two agree (max rel err).  Prints one JSON line; writes profiles/r02_raw_chain.json with --save.
+and checks the two agree (max rel err).  Prints one JSON line (committed as profiles/r02_raw_chain.json).
 """
 import json
 import os
