@@ -575,6 +575,8 @@ struct Chain3 {
   int cpi;                            // chain3v: input chunks per IN item (1 or 2; a 2-chunk item is one
                                       // handoff for two K-steps)
   int NAc;                            // chain3v: conversion-ring slots
+  int NR;                             // chain2h: A2 ring slots (>= the tile's stage-2 items; the extra ones let
+                                      // CONV convert the next tile while this tile's stage 2 still reads A2)
   uint32_t colC;                      // chain3v: conversion ring (A operands of stages 2 and 3)
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
@@ -1492,7 +1494,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       mbar_init(&bars.d3_full[b], 1);
       mbar_init(&bars.d3_free[b], kOUT3);
     }
-    for (int k = 0; k < nk2; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting item k
+    for (int k = 0; k < 16; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting into slot k
     mbar_init(&bars.a2_free, 1);
     for (int k = 0; k < 16; ++k) mbar_init(&bars.a2_ifree[k], 1);
     for (int c = 0; c < p.NAc; ++c) {
@@ -1596,14 +1598,18 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             fence_before();
             warp_arrive(&bars.c_full[slot]);
           } else {
-            if (kA2Item && it > 0) {   // the previous tile's last-shell MMA has read item i
-              role_wait(&bars.a2_ifree[i], (it - 1) & 1);
+            // global item it * nk2 + i lives in A2 ring slot (it * nk2 + i) % NR; its previous occupant must have
+            // been read by the last output shell's MMA
+            const uint32_t gi = it * (uint32_t)nk2 + (uint32_t)i, slot = kA2Item ? gi % (uint32_t)p.NR : (uint32_t)i,
+                           occ = gi / (uint32_t)p.NR;
+            if (kA2Item && occ > 0) {
+              role_wait(&bars.a2_ifree[slot], (occ - 1) & 1);
               fence_after();
             }
-            store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
+            store_parts<PARTS>(tq + p.colA2 + slot * kSlotW, 8, w);
             tmem_wait_st();
             fence_before();
-            warp_arrive(&bars.a2_full[i]);
+            warp_arrive(&bars.a2_full[slot]);
           }
           if (mid && kMidLate) {   // the Gram term planes after the A2 handoff: off the MMA's critical path
             float u[16];
@@ -1893,13 +1899,14 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
           }
           for (int k = 0; k < nk2; ++k) {
+            const uint32_t gi = it * (uint32_t)nk2 + (uint32_t)k, slot = kA2Item ? gi % (uint32_t)p.NR : (uint32_t)k;
             if (o == 0) {
-              mbar_wait_warp(&bars.a2_full[k], it & 1);
+              mbar_wait_warp(&bars.a2_full[slot], (kA2Item ? gi / (uint32_t)p.NR : it) & 1);
               fence_after();
             }
             if (elect_one()) {
-              kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == 0);
-              if (kA2Item && o == p.G2 - 1) commit(&bars.a2_ifree[k]);   // CONV may overwrite item k
+              kstep_ts<PARTS>(d3, tA2 + slot * kSlotW, 8, bd, id2, k == 0);
+              if (kA2Item && o == p.G2 - 1) commit(&bars.a2_ifree[slot]);   // CONV may refill this slot
             }
             __syncwarp();
 #pragma unroll
@@ -2537,6 +2544,11 @@ bool plan_chain2h(Chain3& p, bool kout) {
     if (p.NA < 2) return false;
     if (p.NA > kMaxSlots) p.NA = kMaxSlots;
     p.NAc = 0;
+    // leftover columns become extra A2 ring slots (measurement knob DELIMIT_A2_SPARE caps them)
+    int extra = (spare - p.NA * p.cpi * parts * 8) / (parts * 8);
+    if (const char* e = getenv("DELIMIT_A2_SPARE")) extra = std::min(extra, atoi(e));
+    p.NR = std::min(A2w / (parts * 8) + std::max(extra, 0), 16);
+    A2w = p.NR * parts * 8;
   }
   if (D1w + A2w + D3w + p.NA * p.cpi * parts * 8 > 512) return false;
   p.colA = 0;
