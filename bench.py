@@ -925,24 +925,24 @@ def run_ours(args):
 
     # Dominant-kernel durations inside the timed steps: the library's kernel timer stamps %globaltimer when a
     # launch's first CTA starts and its last CTA ends (device-side, so it works inside the replayed graphs and
-    # times the kernel alone); every timed step's launches are in the ring -- median over them, reconciled with
+    # times the kernel alone); every timed step's launches are in the ring -- mean over them, reconciled with
     # the step time.
     kern = None
     nl = min(args.steps * W.launch_groups, 60)   # the ring holds the last 63 launches per slot
     if W.dom and W.dom[2] is not None:
         try:
-            def med(slot):
+            def med(slot):   # mean over the timed launches (comparable with the mean phase times), then min, max
                 if _lib.ktimer_count(slot) < nl:
                     return None
                 v = [_lib.ktimer_read(slot, b) for b in range(nl)]
-                return statistics.median(v), min(v), max(v)
+                return statistics.mean(v), min(v), max(v)
 
             f, b_, g_ = med(0), med(1), med(2)
             if f:
                 kern = {"fwd_ms": f[0], "fwd_min_max": f[1:],
-                        "how": f"median over the {nl} launches of the timed steps: device %globaltimer stamps at the "
+                        "how": f"mean over the {nl} launches of the timed steps: device %globaltimer stamps at the "
                                f"kernel's first CTA start and last CTA end (inside the replayed graph)" if graphed else
-                               f"median over the {nl} launches of the timed steps: device %globaltimer stamps at the "
+                               f"mean over the {nl} launches of the timed steps: device %globaltimer stamps at the "
                                f"kernel's first CTA start and last CTA end"}
                 if b_:
                     kern["bwd_ms"], kern["bwd_min_max"] = b_[0], b_[1:]
@@ -982,7 +982,7 @@ def run_ours(args):
         dname, dbytes_vox, slot = W.dom
         launch_ms, how = None, None
         if kern and not kern.get("rejected"):
-            launch_ms, how = kern["fwd_ms"], "kernel launches inside the timed steps (device timestamps, median)"
+            launch_ms, how = kern["fwd_ms"], "kernel launches inside the timed steps (device timestamps, mean)"
         else:
             launch_ms = phase_ms.get("fwd", phase_ms.get("step", ms))
             how = "the whole forward phase of the timed step (graph replay; includes small operator kernels)"

@@ -554,7 +554,7 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
 
 // ============================================================================ chain3 kernel
 struct Chain3 {
-  CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
+  CUtensorMap tm[2];                  // channel-pair views of `in` (tm[0]) and the fused-MSE target (tm[1])
   const float* in;
   float* out;
   uint16_t* mid;                      // optional: stage-1 accumulator D1 -> HBM as two bf16 term planes,
@@ -591,6 +591,8 @@ struct Chain3 {
   dl::KTrace* kt;                     // kernel timer (dl_ktimer_*) or null, and its slot
   int kt_slot;
   uint32_t sm_tring;                  // chain2h fused MSE: per-OUT-warp target rings (2 x 16 x 32 fp32), or 0
+  int tg_tma;                         // chain2h fused MSE: the target arrives by TMA (tm[1]) in a shared ring of
+  uint32_t sm_tgring;                 //   kTgStages stages at sm_tgring, loaded by the T-image loader warp
   const void* raw;                    // chain3v raw-acquisition input (in_role_raw) or null
   int raw_type;                       // NIfTI datatype code of raw: 4 int16, 16 float32
   int64_t raw_vstride;                // elements between stored volumes
@@ -1442,9 +1444,11 @@ struct Bars2h {
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
   uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
   uint64_t t_full[2], t_empty[2];                   // tstream: T image buffers
+  uint64_t tg_full[8], tg_empty[8];                 // fused MSE: TMA target ring
   uint32_t tmem_base;
 };
-constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream)
+constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream) + fused-MSE target TMA
+constexpr int kTgStages = 4;                        // fused-MSE target ring stages (16 channels x 132 voxels each)
 constexpr int kThreads2h = (kWT + 1) * 32;
 
 // KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
@@ -1505,6 +1509,10 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.t_full[b], 1);
       mbar_init(&bars.t_empty[b], 1);
+    }
+    for (int b = 0; b < kTgStages; ++b) {
+      mbar_init(&bars.tg_full[b], 1);
+      mbar_init(&bars.tg_empty[b], 4);   // the chunk's four quadrant OUT warps
     }
     mbar_fence_init();
   }
@@ -1640,7 +1648,9 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     // previous chunk's arithmetic and stores instead of stalling them (each thread reads back only what it
     // copied: cp.async.wait_group is the only synchronisation).  Safe when target aliases out: a chunk's
     // target elements are read before that chunk's outputs are written, and chunks never overlap.
-    const bool tring = p.target && p.sm_tring && kOB2h == 1 && !KOUT;
+    const bool tgt = p.target && p.tg_tma && kOB2h == 1 && !KOUT;   // target by TMA (T-image loader warp)
+    const int odd0t = 8 * kBoxV + (int)(p.nvox & 3);                  // odd-channel box offset in a ring stage
+    const bool tring = p.target && p.sm_tring && kOB2h == 1 && !KOUT && !tgt;
     float* tr = reinterpret_cast<float*>(smem + p.sm_tring) + ow * 1024;
     int64_t nt_t = blockIdx.x;   // next target chunk to issue: tile, shell, chunk
     int nt_o = 0, nt_ck = cg;
@@ -1723,6 +1733,31 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
               t_issue();
               cp_async_wait<1>();
               __syncwarp();   // the 8-byte path reads values other lanes copied
+            }
+            if (tgt && ck < nck) {   // fused MSE, TMA target ring: this chunk is chunk n3 * nck + ck of the CTA
+              const uint32_t q = n3 * (uint32_t)nck + (uint32_t)ck, tgs = q % kTgStages;
+              idle_wait<1>(&bars.tg_full[tgs], (q / kTgStages) & 1);
+              const float* rp = reinterpret_cast<const float*>(smem + p.sm_tgring + tgs * kStageBytes) + row;
+              if (ck < nck && vok && p.out) {
+                const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
+                float* d = p.out + off;
+                const int nval = p.C3 - ck * 16;
+                const float* bb = sb + o * p.N3 + ck * 16;
+                float csum = 0.f;   // 16 squares in fp32, then one float64 add per chunk
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  if (nval >= 16 || e < nval) {
+                    const float tv = rp[(e & 1) * odd0t + (e >> 1) * kBoxV];
+                    const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - tv;
+                    csum = fmaf(res, res, csum);
+                    __stcs(d, res * p.out_scale);
+                  }
+                  d += stride;
+                }
+                lacc += (double)csum;
+              }
+              warp_arrive(&bars.tg_empty[tgs]);   // the whole warp, converged
+              continue;
             }
             if (ck >= nck || !vok || !p.out) {
               if (tring && ck < nck) ++tq_use;
@@ -1926,14 +1961,39 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   } else if (warp == kW3LD) {
     if (p.tma)
       tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
-  } else if (p.tstream) {
+  } else if (p.tstream || p.tg_tma) {
     // =========================== T-image loader: shell o's rows of both term images, two buffers ===========
+    // (fused MSE with tg_tma: also the target chunks of each output shell, one shell behind the T images, into the
+    // kTgStages-deep target ring the OUT warps read; chunk q of the CTA-wide sequence (tile, shell, chunk) is in
+    // stage q % kTgStages, consumed by the quadrant warps of group q % 2 -- nck even keeps that fixed)
     const uint32_t tg = (uint32_t)(p.N3 * K2 * 2);
     const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
-    uint32_t n = 0;
-    for (uint32_t it = 0; it < nmine; ++it)
-      for (int o = 0; o < p.G2; ++o, ++n) {
-        const uint32_t b = n & 1;
+    const int nck = p.N3 / 16;
+    uint32_t qtg = 0;
+    if (p.tg_tma && elect_one()) asm volatile("prefetch.tensormap [%0];\n" ::"l"(p.tm + 1) : "memory");
+    __syncwarp();
+    auto target_shell = [&](uint32_t n) {   // target chunks of the CTA's n-th (tile, shell)
+      const uint32_t it = n / (uint32_t)p.G2, o = n - it * (uint32_t)p.G2;
+      const int64_t t = blockIdx.x + (int64_t)it * gridDim.x, b = t / p.tiles_per_b;
+      const int v0 = (int)((t - b * p.tiles_per_b) * kTileV);
+      for (int ck = 0; ck < nck; ++ck, ++qtg) {
+        const uint32_t st = qtg % kTgStages, rd = qtg / kTgStages;
+        if (rd > 0) mbar_wait_warp(&bars.tg_empty[st], (rd - 1) & 1);
+        if (elect_one()) {
+          uint8_t* dst = smem + p.sm_tgring + st * kStageBytes;
+          const int c0 = (int)o * p.C3 + 16 * ck;
+          mbar_arrive_tx(&bars.tg_full[st], kStageBytes);
+          tma_load_3d(dst, p.tm + 1, v0, c0 >> 1, (int)b, &bars.tg_full[st]);
+          tma_load_3d(dst + kStageBytes / 2, p.tm + 1, (int)p.nvox + v0 - (int)(p.nvox & 3), c0 >> 1, (int)b,
+                      &bars.tg_full[st]);
+        }
+        __syncwarp();
+      }
+    };
+    const uint32_t ntot = nmine * (uint32_t)p.G2;
+    for (uint32_t n = 0; n < ntot; ++n) {
+      if (p.tstream) {
+        const uint32_t b = n & 1, o = n % (uint32_t)p.G2;
         if (n >= 2) mbar_wait_warp(&bars.t_empty[b], ((n >> 1) - 1) & 1);
         if (elect_one()) {
           uint8_t* dst = smem + p.sm_w2 + b * 2u * tg;
@@ -1944,6 +2004,9 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
         }
         __syncwarp();
       }
+      if (p.tg_tma && n >= 1) target_shell(n - 1);
+    }
+    if (p.tg_tma && ntot > 0) target_shell(ntot - 1);
   }
   fence_before();
   __syncthreads();
@@ -2565,9 +2628,16 @@ bool plan_chain2h(Chain3& p, bool kout) {
   p.sm_w2 = (uint32_t)o; o = al(o + (p.tstream ? tbufs : (size_t)parts * p.w2_img), 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N3 * 4, 128);
   p.sm_tring = 0;
-  if (p.target && !kout && kOB2h == 1 && !getenv("DELIMIT_NO_TRING")) {   // fused MSE target rings
+  p.sm_tgring = 0;
+  if (p.target && !kout && kOB2h == 1 && p.tg_tma && (p.N3 / 16) % 2 == 0) {   // fused MSE: TMA target ring
+    p.sm_tgring = (uint32_t)o;
+    o = al(o + (size_t)kTgStages * kStageBytes, 128);
+  } else if (p.target && !kout && kOB2h == 1 && !getenv("DELIMIT_NO_TRING")) {   // per-warp cp.async rings
+    p.tg_tma = 0;
     p.sm_tring = (uint32_t)o;
     o = al(o + (size_t)kOUT3 * 2 * 16 * 32 * 4, 128);
+  } else {
+    p.tg_tma = 0;
   }
   p.sm_ring = (uint32_t)o;
   for (int ns : {12, 8, 4}) {
@@ -2962,6 +3032,8 @@ int chain_fwd(const float* x, float* y, void* c_mid, const float* M, int m_per_s
   p.out_scale = out_scale;
   p.loss = loss;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
+  p.tg_tma = target && p.tma && !getenv("DELIMIT_NO_TGTMA") && pair_map(&p.tm[1], target, nbatch, s_out * n_out, n_out, nvox)
+                 ? 1 : 0;
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
   const bool fold = h && use_2h();
   if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, bvec, false, st));
