@@ -88,7 +88,7 @@ def maybe_spawn(args) -> None:
     import torch
 
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and args.dist_backend == "nccl":
         log(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, this box has {have}")
         sys.exit(2)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
@@ -829,10 +829,15 @@ def run_ours(args):
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if torch.cuda.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device")
-    dev = torch.device("cuda", local)
+    # --dist-backend gloo (a test mode): ranks may share GPUs (local rank modulo the visible devices); the kernels of
+    # different ranks never wait on one another -- the only exchange is the host-side all-reduce
+    dev = torch.device("cuda", local % torch.cuda.device_count() if args.dist_backend == "gloo" else local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     W = WORKLOADS[args.config](args, dev, rank, world)
     graphed = W.graphed and not args.no_graph
     flush = _l2_flush_buffer(dev) if W.flush_l2 else None
@@ -898,7 +903,8 @@ def run_ours(args):
     clocks = ClockSampler(uuid) if (rank == 0 and not args.no_clocks) else None
     if clocks:
         clocks.start()
-        for _ in range(max(1, args.warmup)):     # keep the GPU loaded while the sampler spins up
+    if not args.no_clocks:   # every rank (the steps hold collectives): keep the GPU loaded while the sampler spins up
+        for _ in range(max(1, args.warmup)):
             step(False)
     if world > 1:
         dist.barrier()
@@ -1038,6 +1044,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time the eager autograd step instead of CUDA graphs")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: test mode in which ranks may share a GPU (multi-rank logic on a 1-GPU box)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
