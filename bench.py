@@ -66,11 +66,13 @@ def measured_peaks():
         return FALLBACK_HBM, FALLBACK_TF, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """Per-launch DRAM bytes for `kernel` from the committed ncu capture (profiles/ncu_traffic.json), else None."""
+def ncu_traffic(kernel: str, key: str | None = None):
+    """Per-launch DRAM bytes for `kernel` from the committed ncu capture (profiles/ncu_traffic.json), or another of
+    its per-kernel tables (`key`, e.g. tensor_pipe_active_pct), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+            d = json.load(f)
+        return d.get(kernel) if key is None else d.get(key, {}).get(kernel)
     except Exception:
         return None
 
@@ -1004,8 +1006,10 @@ def run_ours(args):
             tflops = W.tensor_flops_per_voxel * V_local / (launch_ms / 1e3) / 1e12
             roof["tensor"] = {"flops_per_launch": W.tensor_flops_per_voxel * V_local, "achieved_tflops": tflops,
                               "peak_tflops": peak_tf, "frac": tflops / peak_tf,
+                              "pipe_active_pct_ncu": ncu_traffic(dname, "tensor_pipe_active_pct"),
                               "note": "MMA flops the kernel issues (fp16 split-term products) over its duration, "
-                                      "against the measured dense bf16 GEMM rate"}
+                                      "against the measured dense bf16 GEMM rate; pipe_active_pct_ncu: "
+                                      "sm__pipe_tensor_cycles_active from the committed ncu capture"}
         step_bytes = W.bytes_per_voxel * W.voxels_per_step() / max(world, 1)
         line = {
             "metric": W.metric, "value": W.voxels_per_step() / (ms / 1e3), "unit": "voxels/s", "n_gpus": world,

@@ -1449,6 +1449,10 @@ struct Bars2h {
 };
 constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream) + fused-MSE target TMA
 constexpr int kTgStages = 4;                        // fused-MSE target ring stages (16 channels x 132 voxels each)
+#ifndef DL_TG_PF
+#define DL_TG_PF 3
+#endif
+constexpr int kTgPf = DL_TG_PF;                     // fused-MSE cp.async rings: chunks of L2 prefetch lead
 constexpr int kThreads2h = (kWT + 1) * 32;
 
 // KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
@@ -1657,8 +1661,33 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     uint32_t tq_issue = 0, tq_use = 0;
     // 8-byte copies (two voxels per lane, two rows per instruction) when every row start is 8-byte aligned
     const bool t8 = (p.nvox % 2 == 0) && ((uintptr_t)p.target % 8 == 0) && (p.out_bs % 2 == 0);
+    // L2 prefetch kTgPf chunks ahead of the copies (lane r < 16: row r's 128-byte segment of this warp's voxels),
+    // so the cp.async of a chunk finds it in L2 instead of waiting out a DRAM latency one chunk before use
+    int64_t pf_t = blockIdx.x;
+    int pf_o = 0, pf_ck = cg;
+    auto pf_advance = [&]() {
+      pf_ck += kOUTQ;
+      if (pf_ck >= nck) {
+        pf_ck = cg;
+        if (++pf_o == p.G2) {
+          pf_o = 0;
+          pf_t += gridDim.x;
+        }
+      }
+    };
+    auto t_prefetch = [&]() {
+      if (kTgPf > 0 && pf_t < ntiles && lane < 16 && lane < p.C3 - pf_ck * 16) {
+        const int64_t bq = pf_t / p.tiles_per_b, v0q = (pf_t - bq * p.tiles_per_b) * kTileV + 32 * qd;
+        if (v0q < p.nvox)
+          prefetch_l2(p.target + bq * p.out_bs + ((int64_t)pf_o * p.C3 + pf_ck * 16 + lane) * stride + v0q);
+      }
+      pf_advance();
+    };
+    if (tring)
+      for (int i = 0; i < kTgPf; ++i) t_prefetch();
     auto t_issue = [&]() {
       __syncwarp();   // every lane has read the stage this copy overwrites (lanes read each other's copies)
+      t_prefetch();
       if (nt_t < ntiles) {
         const int64_t bb_ = nt_t / p.tiles_per_b;
         if (t8) {
