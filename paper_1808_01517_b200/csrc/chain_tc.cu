@@ -1450,9 +1450,9 @@ struct Bars2h {
 constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream) + fused-MSE target TMA
 constexpr int kTgStages = 4;                        // fused-MSE target ring stages (16 channels x 132 voxels each)
 #ifndef DL_TG_PF
-#define DL_TG_PF 3
+#define DL_TG_PF 0
 #endif
-constexpr int kTgPf = DL_TG_PF;                     // fused-MSE cp.async rings: chunks of L2 prefetch lead
+constexpr int kTgPf = DL_TG_PF;   // fused-MSE cp.async rings: chunks of L2 prefetch lead (measured 3: slower; 0 = off)
 constexpr int kThreads2h = (kWT + 1) * 32;
 
 // KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
