@@ -509,7 +509,6 @@ class Cfg5(Workload):
     dom = ("chain_fwd_mse", 2160 + 1080, 0)   # x, target in; dy out
     tensor_flops_per_voxel = Cfg4.tensor_flops_per_voxel
     scaling = "strong"
-    graphed = False
     GLOBAL_BATCH = 8
 
     def __init__(self, args, dev, rank, world):
@@ -538,17 +537,29 @@ class Cfg5(Workload):
     def voxels_per_launch(self):
         return self.V_subject
 
-    def step(self):
-        self.opt.zero_grad(set_to_none=True)
+    def _fwdbwd(self):
+        for p in self.params:
+            p.grad = None
         for x, t in zip(self.xs, self.ts):
             loss = self.net.mse_loss(x, t) * (1.0 / self.GLOBAL_BATCH)
             loss.backward()
+        self.loss = loss
+
+    def step(self):
+        self._fwdbwd()
+        self.after_phases()
+
+    def phases(self):
+        # the forward + backward of every local subject as one CUDA graph; the gradient all-reduce and the SGD update
+        # run after it (eager: the all-reduce is a host-driven collective)
+        return [("fwdbwd", self._fwdbwd)]
+
+    def after_phases(self):
         if self.world > 1:
             from paper_1808_01517_b200.distributed import allreduce_gradients
 
             allreduce_gradients(self.params)
         self.opt.step()
-        self.loss = loss
 
     def config(self):
         return {"workload": "cfg5: Signal2SH(8, 90 dirs, .006) -> LSC 3->3 -> LSC 3->3 ([5], pi/5) -> SH2Signal, MSE "
@@ -558,7 +569,7 @@ class Cfg5(Workload):
                 "model": "SphericalChain (2 LSC layers)", "global_batch": self.GLOBAL_BATCH,
                 "voxels_per_gpu": self.V_local, "subjects_per_gpu": len(self.subjects), "channels": SHELLS * NDIR,
                 "seq_len": None, "parallelism": f"dp{self.world} (subject-sharded, NCCL all_reduce of 114 floats)",
-                "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2", "cuda_graph": False}
+                "l2": "no flush: each input (3.95 GB) exceeds the 126 MB L2"}
 
     def e2e(self):
         """The training step from pinned host x / target buffers (H2D each step), loss read back each step."""

@@ -198,6 +198,15 @@ int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */
 int64_t dl_total_launch_count(void);
 
+/* Small dense float64 products of the stacked-LSC path (csrc/dense.cu): C = alpha op(A) op(B) + beta C with
+ * row-major A (m x k, or k x m when ta), B (k x n, or n x k when tb), C (m x n); and the LSC weight gradient of one
+ * layer from its operator gradient, dW[o,s,k] = sum_{r,t} P[k,r,t] dL[(o,r),(s,t)] -- the folded-layer gradients
+ * of ops.ChainStackFunction (SURVEY.md Appendix A applied per layer; the reference has no backward). */
+int dl_gemm_f64(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, int ta, const double* B, int64_t ldb,
+                int tb, double* C, int64_t ldc, double alpha, double beta, void* stream);
+int dl_lsc_dw_from_dl_f64(const double* dL, const float* P, float* dW, int64_t s_out, int64_t s_in, int64_t K,
+                          int64_t r_out, int64_t r_in, void* stream);
+
 /* Kernel timer (measurement aid for bench.py; no reference counterpart): while armed, the fused chain kernel's
  * fp16-pass launches (slot 0 forward, 1 adjoint) and the LSC weight-gradient Gram launches (slot 2) stamp the
  * device's %globaltimer when their first CTA starts and when their last CTA ends, into a per-slot device ring

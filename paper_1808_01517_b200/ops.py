@@ -95,6 +95,29 @@ def lsc_wgrad(g: torch.Tensor, c: torch.Tensor, fold: torch.Tensor, beta: torch.
     return dW, db
 
 
+def gemm_f64(A: torch.Tensor, B: torch.Tensor, ta: bool = False, tb: bool = False, C: torch.Tensor | None = None,
+             alpha: float = 1.0, beta: float = 0.0) -> torch.Tensor:
+    """C = alpha op(A) op(B) + beta C for small float64 device matrices (dl_gemm_f64, csrc/dense.cu)."""
+    A, B = A.contiguous(), B.contiguous()
+    m, k = (A.shape[1], A.shape[0]) if ta else (A.shape[0], A.shape[1])
+    kb, n = (B.shape[1], B.shape[0]) if tb else (B.shape[0], B.shape[1])
+    if kb != k:
+        raise ShapeError(f"gemm_f64: inner dimensions {k} and {kb} differ")
+    if C is None:
+        C = torch.empty((m, n), dtype=torch.float64, device=A.device)
+        beta = 0.0
+    elif tuple(C.shape) != (m, n) or not C.is_contiguous():
+        raise ShapeError("gemm_f64: C must be a contiguous (m, n) matrix")
+    _lib.call("dl_gemm_f64", m, n, k, _p(A), A.shape[1], int(ta), _p(B), B.shape[1], int(tb), _p(C), n,
+              ctypes.c_double(alpha), ctypes.c_double(beta), _stream())
+    return C
+
+
+def _affine(L: torch.Tensor, d: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """L d + b for float64 device vectors (one dl_gemm_f64 launch)."""
+    return gemm_f64(L, d.reshape(-1, 1), C=b.clone().reshape(-1, 1), beta=1.0).reshape(-1)
+
+
 # ----------------------------------------------------------------------------- autograd
 class ChannelMap(torch.autograd.Function):
     """Per-shell linear map x[s] -> W_s x[s] (Signal2SH: W=M, SH2Signal: W=B'); grad uses W^T."""
@@ -269,15 +292,7 @@ class ChainStackFunction(torch.autograd.Function):
     def forward(ctx, x, M, per_shell, Bt, state_fwd, state_bwd, n_layers, *layers):
         lib = _lib.load()
         ws_ = [layers[4 * i:4 * i + 4] for i in range(n_layers)]
-        Ls, bvecs = [], []
-        for w, b, fold, beta in ws_:
-            L, _, bvec = build_lsc_operator(fold, beta, w, b, want_Lt=False)
-            Ls.append(L.double())
-            bvecs.append(bvec.double())
-        Lt, dt = Ls[0], bvecs[0]
-        for L, bv in zip(Ls[1:], bvecs[1:]):
-            Lt, dt = L @ Lt, L @ dt + bv
-        L_tot, b_tot = Lt.float().contiguous(), dt.float().contiguous()
+        Ls, bvecs, L_tot, b_tot = _fold_layers(ws_)
         w1, f1 = ws_[0][0], ws_[0][2]
         wn, fn = ws_[-1][0], ws_[-1][2]
         s_in, r_in, s_out, r_out = w1.shape[1], f1.shape[2], wn.shape[0], fn.shape[1]
@@ -320,35 +335,18 @@ class ChainStackFunction(torch.autograd.Function):
         g_mid = _workspace(lib.dl_chain_mid_bytes(B, s_out, r_out, V), dy.device)
         _lib.call("dl_chain_bwd_gram_f64", _p(c_mid), _p(dy), _p(dx), _p(G), _p(g_mid), _p(M), int(ctx.per_shell),
                   _p(L_tot), _p(Bt), _p(ws), _p(ctx.state_bwd), B, s_in, s_out, n, r_in, r_out, n_out, V, _stream())
-        rpo, rpi = rows.value // s_out, cols.value // s_in
-        Gr = G.view(s_out, rpo, s_in, rpi)[:, :r_out, :, :r_in].reshape(s_out * r_out, s_in * r_in)
-        sv = G.view(s_out, rpo, cols.value)[:, :r_out, r_in].reshape(-1)
-        Ls, bvecs = ctx.Ls, ctx.bvecs
-        # C_{k-1}, d_{k-1} (input side) and A_k (output side) of every layer
-        Cs, ds = [None] * nl, [None] * nl
-        C = torch.eye(s_in * r_in, dtype=torch.float64, device=dy.device)
-        d = torch.zeros(s_in * r_in, dtype=torch.float64, device=dy.device)
-        for k in range(nl):
-            Cs[k], ds[k] = C, d
-            C, d = Ls[k] @ C, Ls[k] @ d + bvecs[k]
+        grads = _layer_grads(G, rows.value, cols.value, (s_in, s_out, r_in, r_out, nl), ctx.Ls, ctx.bvecs, lay,
+                             ctx.has_bias, dy.device)
         out = list(nones)
         out[0] = dx if ctx.needs_input_grad[0] else None
-        A = torch.eye(s_out * r_out, dtype=torch.float64, device=dy.device)
-        for k in reversed(range(nl)):
-            w, fold, beta = lay[3 * k], lay[3 * k + 1], lay[3 * k + 2]
-            so, si, K = w.shape
-            ro, ri = fold.shape[1], fold.shape[2]
-            gs = A @ sv
-            dL = (A @ Gr @ Cs[k].T + torch.outer(gs, ds[k])).view(so, ro, si, ri)
-            out[7 + 4 * k] = torch.einsum("krt,orst->osk", fold.double(), dL).float()
-            if ctx.has_bias[k]:
-                out[7 + 4 * k + 1] = (gs.view(so, ro) @ beta.double()).float()
-            A = Ls[k].T @ A
+        for k in range(nl):
+            out[7 + 4 * k] = grads[2 * k]
+            out[7 + 4 * k + 1] = grads[2 * k + 1]
         return tuple(out)
 
 
 def _fold_layers(layers):
-    """Per-layer (L_k, bvec_k) in float64 and the product L = L_n ... L_1 with its folded bias."""
+    """Per-layer (L_k, bvec_k) in float64 and the product L = L_n ... L_1 with its folded bias (dl_gemm_f64)."""
     Ls, bvecs = [], []
     for w, b, fold, beta in layers:
         L, _, bvec = build_lsc_operator(fold, beta, w, b, want_Lt=False)
@@ -356,34 +354,40 @@ def _fold_layers(layers):
         bvecs.append(bvec.double())
     Lt, dt = Ls[0], bvecs[0]
     for L, bv in zip(Ls[1:], bvecs[1:]):
-        Lt, dt = L @ Lt, L @ dt + bv
+        Lt, dt = gemm_f64(L, Lt), _affine(L, dt, bv)
     return Ls, bvecs, Lt.float().contiguous(), dt.float().contiguous()
 
 
 def _layer_grads(G, rows, cols, dims, Ls, bvecs, lay, has_bias, device):
-    """Per-layer dW / db from the float64 Gram (see ChainStackFunction); `lay` = (w, fold, beta) per layer."""
+    """Per-layer dW / db from the float64 Gram (see ChainStackFunction); `lay` = (w, fold, beta) per layer.
+    dL_k = A_k G C_{k-1}^T + (A_k s) d_{k-1}^T by dl_gemm_f64, dW_k = <P_k, dL_k> by dl_lsc_dw_from_dl_f64."""
     s_in, s_out, r_in, r_out, nl = dims
     rpo, rpi = rows // s_out, cols // s_in
-    Gr = G.view(s_out, rpo, s_in, rpi)[:, :r_out, :, :r_in].reshape(s_out * r_out, s_in * r_in)
-    sv = G.view(s_out, rpo, cols)[:, :r_out, r_in].reshape(-1)
+    Gr = G.view(s_out, rpo, s_in, rpi)[:, :r_out, :, :r_in].reshape(s_out * r_out, s_in * r_in).contiguous()
+    sv = G.view(s_out, rpo, cols)[:, :r_out, r_in].reshape(-1).contiguous()
     Cs, ds = [None] * nl, [None] * nl
     C = torch.eye(s_in * r_in, dtype=torch.float64, device=device)
     d = torch.zeros(s_in * r_in, dtype=torch.float64, device=device)
     for k in range(nl):
         Cs[k], ds[k] = C, d
-        C, d = Ls[k] @ C, Ls[k] @ d + bvecs[k]
+        if k + 1 < nl:
+            C, d = gemm_f64(Ls[k], C), _affine(Ls[k], d, bvecs[k])
     out = [None] * (2 * nl)
     A = torch.eye(s_out * r_out, dtype=torch.float64, device=device)
     for k in reversed(range(nl)):
         w, fold, beta = lay[3 * k], lay[3 * k + 1], lay[3 * k + 2]
         so, si, K = w.shape
         ro, ri = fold.shape[1], fold.shape[2]
-        gs = A @ sv
-        dL = (A @ Gr @ Cs[k].T + torch.outer(gs, ds[k])).view(so, ro, si, ri)
-        out[2 * k] = torch.einsum("krt,orst->osk", fold.double(), dL).float()
+        gs = gemm_f64(A, sv.reshape(-1, 1)).reshape(-1)
+        dL = gemm_f64(gemm_f64(A, Gr), Cs[k], tb=True)
+        dL = gemm_f64(gs.reshape(-1, 1), ds[k].reshape(1, -1), C=dL, beta=1.0)
+        dW = torch.empty((so, si, K), dtype=torch.float32, device=device)
+        _lib.call("dl_lsc_dw_from_dl_f64", _p(dL), _p(fold), _p(dW), so, si, K, ro, ri, _stream())
+        out[2 * k] = dW
         if has_bias[k]:
-            out[2 * k + 1] = (gs.view(so, ro) @ beta.double()).float()
-        A = Ls[k].T @ A
+            out[2 * k + 1] = gemm_f64(gs.reshape(so, ro), beta.double().reshape(-1, 1)).reshape(-1).float()
+        if k > 0:
+            A = gemm_f64(Ls[k], A, ta=True)
     return out
 
 
