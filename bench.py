@@ -103,7 +103,7 @@ def maybe_spawn(args) -> None:
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, uuid: str | None):
         self.proc = None
@@ -128,24 +128,33 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw, plim = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) != 6:
+            if len(parts) != 8:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:]):
+            for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+            try:
+                pw.append(float(parts[6]))
+                plim = float(parts[7])
+            except ValueError:
+                pass
         if not sm:
             return None
         loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        res = {"sm_mhz": statistics.median(loaded), "sm_min_mhz": min(loaded), "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:
+            res.update(power_w_median=statistics.median(pw), power_w_max=max(pw), power_limit_w=plim)
+        return res
 
 
 # ----------------------------------------------------------------------------- synthetic inputs
