@@ -103,7 +103,8 @@ def maybe_spawn(args) -> None:
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,power.limit")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,power.limit,"
+              "clocks.mem")
 
     def __init__(self, uuid: str | None):
         self.proc = None
@@ -128,11 +129,11 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons, pw, plim = [], None, set(), [], None
+        sm, mx, reasons, pw, plim, mem = [], None, set(), [], None, []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) != 8:
+            if len(parts) != 9:
                 continue
             try:
                 sm.append(float(parts[0]))
@@ -145,6 +146,7 @@ class ClockSampler:
             try:
                 pw.append(float(parts[6]))
                 plim = float(parts[7])
+                mem.append(float(parts[8]))
             except ValueError:
                 pass
         if not sm:
@@ -154,6 +156,8 @@ class ClockSampler:
                "reasons": sorted(reasons), "samples": len(sm)}
         if pw:
             res.update(power_w_median=statistics.median(pw), power_w_max=max(pw), power_limit_w=plim)
+        if mem:
+            res.update(mem_mhz=statistics.median(mem))
         return res
 
 

@@ -198,6 +198,19 @@ int dl_last_launch_count(void);
 /* Kernel launches enqueued by this library since it was loaded (all threads). */
 int64_t dl_total_launch_count(void);
 
+/* Fused Signal2SH -> SH2Signal round trip (fitting.py:206-250 composed; acceptance criterion 1): the chain kernels
+ * with the identity as the LSC operator (built in the workspace) and a block-diagonal stage 2 (output shell s reads
+ * only shell s's coefficients, which never reach memory).  Forward y[s] = B' M_s x[s]; backward dx[s] = M_s^T B'^T dy[s].
+ * workspace: dl_round_trip_workspace_bytes; state as for dl_chain_fwd_f32 (one per direction). */
+size_t dl_round_trip_workspace_bytes(int64_t nbatch, int64_t shells, int64_t n, int64_t r, int64_t n_out,
+                                     int64_t nvox);
+int dl_round_trip_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, const float* Bt, void* workspace,
+                          void* state, int64_t nbatch, int64_t shells, int64_t n, int64_t r, int64_t n_out,
+                          int64_t nvox, void* stream);
+int dl_round_trip_bwd_f32(const float* dy, float* dx, const float* M, int m_per_shell, const float* Bt,
+                          void* workspace, void* state, int64_t nbatch, int64_t shells, int64_t n, int64_t r,
+                          int64_t n_out, int64_t nvox, void* stream);
+
 /* Small dense float64 products of the stacked-LSC path (csrc/dense.cu): C = alpha op(A) op(B) + beta C with
  * row-major A (m x k, or k x m when ta), B (k x n, or n x k when tb), C (m x n); and the LSC weight gradient of one
  * layer from its operator gradient, dW[o,s,k] = sum_{r,t} P[k,r,t] dL[(o,r),(s,t)] -- the folded-layer gradients

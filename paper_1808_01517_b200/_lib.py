@@ -51,6 +51,9 @@ SIGNATURES = {
     "dl_normalize_b0_f32": (_int, [_c_p, _int] + [_i64] * 7 + [ctypes.c_double] * 2
                             + [_c_p, _i64, _c_p, _i64, _c_p, _c_p, _c_p, _c_p]),
     "dl_chain_fwd_raw_f32": (_int, [_c_p, _int, _i64] + [_c_p] * 5 + [_int] + [_c_p] * 5 + [_i64] * 7 + [_c_p]),
+    "dl_round_trip_workspace_bytes": (_size, [_i64] * 6),
+    "dl_round_trip_fwd_f32": (_int, [_c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p] + [_i64] * 6 + [_c_p]),
+    "dl_round_trip_bwd_f32": (_int, [_c_p, _c_p, _c_p, _int, _c_p, _c_p, _c_p] + [_i64] * 6 + [_c_p]),
     "dl_gemm_f64": (_int, [_i64, _i64, _i64, _c_p, _i64, _int, _c_p, _i64, _int, _c_p, _i64, ctypes.c_double,
                             ctypes.c_double, _c_p]),
     "dl_lsc_dw_from_dl_f64": (_int, [_c_p, _c_p, _c_p] + [_i64] * 5 + [_c_p]),

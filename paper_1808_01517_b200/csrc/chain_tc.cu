@@ -575,6 +575,8 @@ struct Chain3 {
   int cpi;                            // chain3v: input chunks per IN item (1 or 2; a 2-chunk item is one
                                       // handoff for two K-steps)
   int NAc;                            // chain3v: conversion-ring slots
+  int t_diag;                         // chain2h: T block-diagonal over shells (round trip, L = I): output shell o
+                                      // reads only input group o's A2 items
   int NR;                             // chain2h: A2 ring slots (>= the tile's stage-2 items; the extra ones let
                                       // CONV convert the next tile while this tile's stage 2 still reads A2)
   uint32_t colC;                      // chain3v: conversion ring (A operands of stages 2 and 3)
@@ -1962,15 +1964,19 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
 #pragma unroll
             for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
           }
-          for (int k = 0; k < nk2; ++k) {
+          // block-diagonal T (round trip): only input group o's items, each read by this shell alone
+          const int kb = p.t_diag ? o * (nk2 / p.G2) : 0, ke = p.t_diag ? kb + nk2 / p.G2 : nk2;
+#pragma unroll
+          for (int j = 0; j < PARTS; ++j) bd[j] += (uint64_t)kb * ks2;
+          for (int k = kb; k < ke; ++k) {
             const uint32_t gi = it * (uint32_t)nk2 + (uint32_t)k, slot = kA2Item ? gi % (uint32_t)p.NR : (uint32_t)k;
-            if (o == 0) {
+            if (o == 0 || p.t_diag) {
               mbar_wait_warp(&bars.a2_full[slot], (kA2Item ? gi / (uint32_t)p.NR : it) & 1);
               fence_after();
             }
             if (elect_one()) {
-              kstep_ts<PARTS>(d3, tA2 + slot * kSlotW, 8, bd, id2, k == 0);
-              if (kA2Item && o == p.G2 - 1) commit(&bars.a2_ifree[slot]);   // CONV may refill this slot
+              kstep_ts<PARTS>(d3, tA2 + slot * kSlotW, 8, bd, id2, k == kb);
+              if (kA2Item && (o == p.G2 - 1 || p.t_diag)) commit(&bars.a2_ifree[slot]);   // CONV may refill the slot
             }
             __syncwarp();
 #pragma unroll
@@ -3029,7 +3035,7 @@ namespace {
 int chain_fwd(const float* x, float* y, void* c_mid, const float* M, int m_per_shell, const float* L,
               const float* bvec, const float* Bt, void* workspace, void* state, int64_t nbatch, int64_t s_in,
               int64_t s_out, int64_t n, int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream,
-              const float* target, float out_scale, double* loss) {
+              const float* target, float out_scale, double* loss, int diag = 0) {
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
   DL_REQUIRE(x && y && M && L && Bt && workspace, "chain_fwd: null pointer");
@@ -3061,6 +3067,7 @@ int chain_fwd(const float* x, float* y, void* c_mid, const float* M, int m_per_s
   p.out_scale = out_scale;
   p.loss = loss;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
+  p.t_diag = diag;
   // fused MSE target by TMA (measured 4.17 vs 4.04 ms for the per-warp cp.async rings at cfg5: a knob, off)
   p.tg_tma = target && p.tma && getenv("DELIMIT_TGTMA") && pair_map(&p.tm[1], target, nbatch, s_out * n_out, n_out, nvox)
                  ? 1 : 0;
@@ -3182,7 +3189,7 @@ namespace {
 int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* db, double* gram_out, void* g_mid,
               const float* M, int m_per_shell, const float* L, const float* Bt, const float* P, const float* beta,
               void* workspace, void* state, int64_t nbatch, int64_t s_in, int64_t s_out, int64_t K, int64_t n,
-              int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream) {
+              int64_t r_in, int64_t r_out, int64_t n_out, int64_t nvox, void* stream, int diag = 0) {
   int sm = 0;
   DL_TRY(dl::device_check(&sm));
   DL_REQUIRE(dy && M && L && Bt && workspace, "chain_bwd: null pointer");
@@ -3209,6 +3216,7 @@ int chain_bwd(const void* c_mid, const float* dy, float* dx, float* dW, float* d
     p.mid_ones = -1;
     p.bias2 = nullptr;
     p.tma = !tma_disabled() && pair_map(&p.tm[0], dy, nbatch, s_out * n_out, n_out, nvox);
+    p.t_diag = diag;
     // adjoint: stage 1 uses B' (w1 = imgB), stage 3 uses M (w3 = imgM)
     const bool fold = h && use_2h();
     if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, nullptr, true, st));
@@ -3278,6 +3286,62 @@ int dl_chain_gram_dims(int64_t s_in, int64_t s_out, int64_t r_in, int64_t r_out,
   *rows = s_out * ((r_out + 15) / 16 * 16);
   *cols = s_in * ((r_in + 15) / 16 * 16);
   return DL_OK;
+}
+
+}  // extern "C"
+
+namespace dl {
+namespace tc {
+namespace {
+__global__ void eye_k(float* L, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x)
+    L[e] = (e / n == e % n) ? 1.f : 0.f;
+}
+// the identity standing in for the LSC operator of the round trip, at the end of the caller's workspace
+float* round_trip_eye(void* workspace, int64_t s, int64_t r, int64_t n, int64_t n_out, int64_t nvox, cudaStream_t st,
+                      int* status) {
+  const size_t off = al(ws_layout(make_dims(1, s, s, n, r, r, n_out, nvox, 1), kMaxParts).total, 256);
+  float* eye = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + off);
+  const int m = (int)(s * r);
+  eye_k<<<(m * m + 255) / 256 < 256 ? (m * m + 255) / 256 : 256, 256, 0, st>>>(eye, m);
+  *status = dl::after_launch("round_trip_eye");
+  return eye;
+}
+}  // namespace
+}  // namespace tc
+}  // namespace dl
+
+extern "C" {
+
+size_t dl_round_trip_workspace_bytes(int64_t nbatch, int64_t shells, int64_t n, int64_t r, int64_t n_out,
+                                     int64_t nvox) {
+  using namespace dl::tc;
+  return al(ws_layout(make_dims(nbatch, shells, shells, n, r, r, n_out, nvox, 1), kMaxParts).total, 256) +
+         (size_t)(shells * r) * (size_t)(shells * r) * 4;
+}
+
+int dl_round_trip_fwd_f32(const float* x, float* y, const float* M, int m_per_shell, const float* Bt, void* workspace,
+                          void* state, int64_t nbatch, int64_t shells, int64_t n, int64_t r, int64_t n_out,
+                          int64_t nvox, void* stream) {
+  dl::begin_call();
+  DL_REQUIRE(workspace, "round_trip_fwd: null workspace");
+  int st = DL_OK;
+  const float* eye = dl::tc::round_trip_eye(workspace, shells, r, n, n_out, nvox, dl::as_stream(stream), &st);
+  DL_TRY(st);
+  return dl::tc::chain_fwd(x, y, nullptr, M, m_per_shell, eye, nullptr, Bt, workspace, state, nbatch, shells, shells,
+                           n, r, r, n_out, nvox, stream, nullptr, 0.f, nullptr, 1);
+}
+
+int dl_round_trip_bwd_f32(const float* dy, float* dx, const float* M, int m_per_shell, const float* Bt,
+                          void* workspace, void* state, int64_t nbatch, int64_t shells, int64_t n, int64_t r,
+                          int64_t n_out, int64_t nvox, void* stream) {
+  dl::begin_call();
+  DL_REQUIRE(workspace, "round_trip_bwd: null workspace");
+  int st = DL_OK;
+  const float* eye = dl::tc::round_trip_eye(workspace, shells, r, n, n_out, nvox, dl::as_stream(stream), &st);
+  DL_TRY(st);
+  return dl::tc::chain_bwd(nullptr, dy, dx, nullptr, nullptr, nullptr, nullptr, M, m_per_shell, eye, Bt, nullptr,
+                           nullptr, workspace, state, nbatch, shells, shells, 1, n, r, r, n_out, nvox, stream, 1);
 }
 
 }  // extern "C"

@@ -329,7 +329,6 @@ class RoundTrip(nn.Module):
         if s2sh.sh_order != sh2s.sh_order:
             raise ShapeError(f"Signal2SH order {s2sh.sh_order} does not match SH2Signal order {sh2s.sh_order}")
         self.s2sh, self.sh2s = s2sh, sh2s
-        self._eye = {}
         self._state = {}
         self._fused = {}
 
@@ -354,10 +353,5 @@ class RoundTrip(nn.Module):
         x = ops.as_device_f32(x, "signal")
         if not self.fused(s):
             return self.sh2s(self.s2sh(x))
-        n = s * self.s2sh.n_coeffs
-        key = (str(x.device), n)
-        if key not in self._eye:
-            self._eye[key] = torch.eye(n, dtype=torch.float32, device=x.device)
         sf, sb = self.range_state(x.device)
-        return ops.RoundTripFunction.apply(x, self.s2sh.fit_matrix, self.s2sh.per_shell, self.sh2s.basis,
-                                           self._eye[key], sf, sb)
+        return ops.RoundTripFunction.apply(x, self.s2sh.fit_matrix, self.s2sh.per_shell, self.sh2s.basis, s, sf, sb)

@@ -233,31 +233,30 @@ class ChainFunction(torch.autograd.Function):
 
 
 class RoundTripFunction(torch.autograd.Function):
-    """Fused Signal2SH -> SH2Signal (dl_chain_fwd_f32 / dl_chain_bwd_f32 with L = I, no bias, no Gram).
+    """Fused Signal2SH -> SH2Signal (dl_round_trip_fwd_f32 / dl_round_trip_bwd_f32).
 
-    y[s] = B' M_s x[s] (fitting.py:206-250 composed): the coefficients c = M x stay in TMEM; the backward is the
-    adjoint pass dx = M_s^T B'^T dy.  `eye` is the (S*R) x (S*R) identity standing in for the LSC operator.
+    y[s] = B' M_s x[s] (fitting.py:206-250 composed): the coefficients c = M x stay in TMEM and the stage-2 product
+    is block-diagonal over shells; the backward is the adjoint pass dx = M_s^T B'^T dy.
     """
 
     @staticmethod
-    def forward(ctx, x, M, per_shell, Bt, eye, state_fwd, state_bwd):
+    def forward(ctx, x, M, per_shell, Bt, shells, state_fwd, state_bwd):
         r, n = M.shape[-2], M.shape[-1]
         n_out = Bt.shape[0]
-        s = eye.shape[0] // r
         B, V = x.shape[0], nvox_of(x)
         lib = _lib.load()
-        y = torch.empty((B, s * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
-        ws = _workspace(lib.dl_chain_workspace_bytes(B, s, s, n, r, r, n_out, V), x.device)
-        _lib.call("dl_chain_fwd_f32", _p(x), _p(y), _NULL, _p(M), int(per_shell), _p(eye), _NULL, _p(Bt), _p(ws),
-                  _p(state_fwd), B, s, s, n, r, r, n_out, V, _stream())
-        ctx.save_for_backward(M, Bt, eye)
+        y = torch.empty((B, shells * n_out, *x.shape[2:]), dtype=torch.float32, device=x.device)
+        ws = _workspace(lib.dl_round_trip_workspace_bytes(B, shells, n, r, n_out, V), x.device)
+        _lib.call("dl_round_trip_fwd_f32", _p(x), _p(y), _p(M), int(per_shell), _p(Bt), _p(ws), _p(state_fwd), B,
+                  shells, n, r, n_out, V, _stream())
+        ctx.save_for_backward(M, Bt)
         ctx.per_shell, ctx.state_bwd = per_shell, state_bwd
-        ctx.shape = (B, V, tuple(x.shape), s)
+        ctx.shape = (B, V, tuple(x.shape), shells)
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        M, Bt, eye = ctx.saved_tensors
+        M, Bt = ctx.saved_tensors
         B, V, xshape, s = ctx.shape
         if not ctx.needs_input_grad[0]:
             return (None,) * 7
@@ -266,9 +265,9 @@ class RoundTripFunction(torch.autograd.Function):
         dy = as_device_f32(dy, "grad")
         lib = _lib.load()
         dx = torch.empty(xshape, dtype=torch.float32, device=dy.device)
-        ws = _workspace(lib.dl_chain_workspace_bytes(B, s, s, n, r, r, n_out, V), dy.device)
-        _lib.call("dl_chain_bwd_f32", _NULL, _p(dy), _p(dx), _NULL, _NULL, _NULL, _p(M), int(ctx.per_shell), _p(eye),
-                  _p(Bt), _NULL, _NULL, _p(ws), _p(ctx.state_bwd), B, s, s, 1, n, r, r, n_out, V, _stream())
+        ws = _workspace(lib.dl_round_trip_workspace_bytes(B, s, n, r, n_out, V), dy.device)
+        _lib.call("dl_round_trip_bwd_f32", _p(dy), _p(dx), _p(M), int(ctx.per_shell), _p(Bt), _p(ws), _p(ctx.state_bwd),
+                  B, s, n, r, n_out, V, _stream())
         return dx, None, None, None, None, None, None
 
 
