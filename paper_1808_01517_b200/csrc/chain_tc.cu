@@ -1425,6 +1425,7 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #define DL_OB2H 1
 #endif
 constexpr int kOB2h = DL_OB2H;   // D3 chunks an OUT warp loads before releasing / storing them
+constexpr int kTgStagesMax = 4;
 // A2 released item by item as the last output shell's stage-2 MMAs read it (a2_ifree), so CONV converts the
 // next tile's items while that shell's MMAs still run; 0: one a2_free for the whole tile (measurement knob)
 #ifndef DL_A2_ITEM
@@ -1436,8 +1437,11 @@ constexpr bool kA2Item = DL_A2_ITEM != 0;
 #define DL_MID_LATE 1
 #endif
 constexpr bool kMidLate = DL_MID_LATE != 0;
+// chain2h keeps its barriers small: with the 12-deep TMA ring the shared-memory plan has < 900 bytes left for
+// them (a larger block silently drops the ring to 8 stages)
+constexpr int kMaxStages2h = 12;
 struct Bars2h {
-  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t full[kMaxStages2h], empty[kMaxStages2h];
   uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
   uint64_t d1g_full[2], d1g_free[2];
   uint64_t a2_full[16], a2_free;
@@ -1446,11 +1450,11 @@ struct Bars2h {
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
   uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
   uint64_t t_full[2], t_empty[2];                   // tstream: T image buffers
-  uint64_t tg_full[8], tg_empty[8];                 // fused MSE: TMA target ring
+  uint64_t tg_full[kTgStagesMax], tg_empty[kTgStagesMax];   // fused MSE: TMA target ring
   uint32_t tmem_base;
 };
 constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream) + fused-MSE target TMA
-constexpr int kTgStages = 4;                        // fused-MSE target ring stages (16 channels x 132 voxels each)
+constexpr int kTgStages = kTgStagesMax;             // fused-MSE target ring stages (16 channels x 132 voxels each)
 #ifndef DL_TG_PF
 #define DL_TG_PF 0
 #endif

@@ -8,8 +8,8 @@ for r in $(seq 1 $R); do
   for spec in $1; do
     t=${spec%%:*}; envs=""
     [[ "$spec" == *:* ]] && envs=$(echo "${spec#*:}" | tr ',' ' ')
-    env $envs DELIMIT_LIB=paper_1808_01517_b200/libdelimit_$t.so timeout 300 python bench.py --steps 10 --warmup 3 \
+    env $envs DELIMIT_LIB=paper_1808_01517_b200/libdelimit_$t.so timeout 300 python bench.py ${AB_STEPS:---steps 10 --warmup 3} \
       --no-e2e --no-cpu $AB_ARGS > gpurun_out/ab_$r.json 2>/dev/null
-    python -c "import json;d=json.load(open('gpurun_out/ab_$r.json'));k=d.get('kernel_ms') or {};print('$spec', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phase_ms'].items()}, 'kern', [round(k.get(x,0),3) for x in ('fwd_ms','bwd_ms','gram_ms')], d['clocks']['sm_mhz'])" 2>&1 | tail -1
+    python -c "import json;d=json.load(open('gpurun_out/ab_$r.json'));k=d.get('kernel_ms') or {};print('$spec', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phase_ms'].items()}, 'kern', [round(k.get(x,0),3) for x in ('fwd_ms','bwd_ms','gram_ms')], d['clocks']['sm_mhz'], d['clocks'].get('sm_min_mhz'))" 2>&1 | tail -1
   done
 done
