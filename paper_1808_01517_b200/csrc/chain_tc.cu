@@ -554,7 +554,7 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
 
 // ============================================================================ chain3 kernel
 struct Chain3 {
-  CUtensorMap tm[2];                  // channel-pair views of `in` (tm[0]) and the fused-MSE target (tm[1])
+  CUtensorMap tm[2];                  // channel-pair view of `in` (tm[1] unused)
   const float* in;
   float* out;
   uint16_t* mid;                      // optional: stage-1 accumulator D1 -> HBM as two bf16 term planes,
@@ -576,9 +576,8 @@ struct Chain3 {
                                       // handoff for two K-steps)
   int NAc;                            // chain3v: conversion-ring slots
   int t_diag;                         // chain2h: T block-diagonal over shells (round trip, L = I): output shell o
-                                      // reads only input group o's A2 items
-  int NR;                             // chain2h: A2 ring slots (>= the tile's stage-2 items; the extra ones let
-                                      // CONV convert the next tile while this tile's stage 2 still reads A2)
+                                      // reads only input group o's A2 items (the 12-stage instantiation; the
+                                      // others run the dense T, exact as well)
   uint32_t colC;                      // chain3v: conversion ring (A operands of stages 2 and 3)
   uint32_t w1_img, w2_img, w3_img;    // bytes per image
   uint32_t sm_w1, sm_w2, sm_w3, sm_bias, sm_ring, sm_bar, smem_bytes;
@@ -593,8 +592,6 @@ struct Chain3 {
   dl::KTrace* kt;                     // kernel timer (dl_ktimer_*) or null, and its slot
   int kt_slot;
   uint32_t sm_tring;                  // chain2h fused MSE: per-OUT-warp target rings (2 x 16 x 32 fp32), or 0
-  int tg_tma;                         // chain2h fused MSE: the target arrives by TMA (tm[1]) in a shared ring of
-  uint32_t sm_tgring;                 //   kTgStages stages at sm_tgring, loaded by the T-image loader warp
   const void* raw;                    // chain3v raw-acquisition input (in_role_raw) or null
   int raw_type;                       // NIfTI datatype code of raw: 4 int16, 16 float32
   int64_t raw_vstride;                // elements between stored volumes
@@ -1425,7 +1422,6 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
 #define DL_OB2H 1
 #endif
 constexpr int kOB2h = DL_OB2H;   // D3 chunks an OUT warp loads before releasing / storing them
-constexpr int kTgStagesMax = 4;
 // A2 released item by item as the last output shell's stage-2 MMAs read it (a2_ifree), so CONV converts the
 // next tile's items while that shell's MMAs still run; 0: one a2_free for the whole tile (measurement knob)
 #ifndef DL_A2_ITEM
@@ -1450,22 +1446,16 @@ struct Bars2h {
   uint64_t c_full[kMaxSlots], c_empty[kMaxSlots];   // KOUT: A2 item ring
   uint64_t d3g_free[4];                             // KOUT: output shell o of D3 drained
   uint64_t t_full[2], t_empty[2];                   // tstream: T image buffers
-  uint64_t tg_full[kTgStagesMax], tg_empty[kTgStagesMax];   // fused MSE: TMA target ring
   uint32_t tmem_base;
 };
-constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream) + fused-MSE target TMA
-constexpr int kTgStages = kTgStagesMax;             // fused-MSE target ring stages (16 channels x 132 voxels each)
-#ifndef DL_TG_PF
-#define DL_TG_PF 0
-#endif
-constexpr int kTgPf = DL_TG_PF;   // fused-MSE cp.async rings: chunks of L2 prefetch lead (measured 3: slower; 0 = off)
+constexpr int kWT = kW3LD + 1;                      // chain2h: T-image loader warp (tstream)
 constexpr int kThreads2h = (kWT + 1) * 32;
 
 // KOUT = false: A2 resident, stage 2 one output shell at a time (D3 double-buffered).
 // KOUT = true: A2 items stream through a ring (NAc slots) and stage 2 is K-outer over all output shells
 //   (D3 holds every shell; OUT releases shell o as soon as it is drained, so the next tile's first K-step
 //   into shell o can start), which removes the CONV -> stage 2 -> a2_free -> CONV cycle of the tile.
-template <int NS, bool KOUT>
+template <int NS, bool KOUT, bool DIAG>
 __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
   constexpr int PARTS = 2;
   constexpr bool H = true;
@@ -1508,7 +1498,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
       mbar_init(&bars.d3_full[b], 1);
       mbar_init(&bars.d3_free[b], kOUT3);
     }
-    for (int k = 0; k < 16; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting into slot k
+    for (int k = 0; k < nk2; ++k) mbar_init(&bars.a2_full[k], 4);   // the quadrant warps converting item k
     mbar_init(&bars.a2_free, 1);
     for (int k = 0; k < 16; ++k) mbar_init(&bars.a2_ifree[k], 1);
     for (int c = 0; c < p.NAc; ++c) {
@@ -1519,10 +1509,6 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.t_full[b], 1);
       mbar_init(&bars.t_empty[b], 1);
-    }
-    for (int b = 0; b < kTgStages; ++b) {
-      mbar_init(&bars.tg_full[b], 1);
-      mbar_init(&bars.tg_empty[b], 4);   // the chunk's four quadrant OUT warps
     }
     mbar_fence_init();
   }
@@ -1616,18 +1602,16 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             fence_before();
             warp_arrive(&bars.c_full[slot]);
           } else {
-            // global item it * nk2 + i lives in A2 ring slot (it * nk2 + i) % NR; its previous occupant must have
-            // been read by the last output shell's MMA
-            const uint32_t gi = it * (uint32_t)nk2 + (uint32_t)i, slot = kA2Item ? gi % (uint32_t)p.NR : (uint32_t)i,
-                           occ = gi / (uint32_t)p.NR;
-            if (kA2Item && occ > 0) {
-              role_wait(&bars.a2_ifree[slot], (occ - 1) & 1);
+            // the previous tile's item i was read by its last reader (the last output shell's MMA, or shell i's
+            // group alone for a block-diagonal T)
+            if (kA2Item && it > 0) {
+              role_wait(&bars.a2_ifree[i], (it - 1) & 1);
               fence_after();
             }
-            store_parts<PARTS>(tq + p.colA2 + slot * kSlotW, 8, w);
+            store_parts<PARTS>(tq + p.colA2 + (uint32_t)i * kSlotW, 8, w);
             tmem_wait_st();
             fence_before();
-            warp_arrive(&bars.a2_full[slot]);
+            warp_arrive(&bars.a2_full[i]);
           }
           if (mid && kMidLate) {   // the Gram term planes after the A2 handoff: off the MMA's critical path
             float u[16];
@@ -1658,42 +1642,15 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     // previous chunk's arithmetic and stores instead of stalling them (each thread reads back only what it
     // copied: cp.async.wait_group is the only synchronisation).  Safe when target aliases out: a chunk's
     // target elements are read before that chunk's outputs are written, and chunks never overlap.
-    const bool tgt = p.target && p.tg_tma && kOB2h == 1 && !KOUT;   // target by TMA (T-image loader warp)
-    const int odd0t = 8 * kBoxV + (int)(p.nvox & 3);                  // odd-channel box offset in a ring stage
-    const bool tring = p.target && p.sm_tring && kOB2h == 1 && !KOUT && !tgt;
+    const bool tring = p.target && p.sm_tring && kOB2h == 1 && !KOUT;
     float* tr = reinterpret_cast<float*>(smem + p.sm_tring) + ow * 1024;
     int64_t nt_t = blockIdx.x;   // next target chunk to issue: tile, shell, chunk
     int nt_o = 0, nt_ck = cg;
     uint32_t tq_issue = 0, tq_use = 0;
     // 8-byte copies (two voxels per lane, two rows per instruction) when every row start is 8-byte aligned
     const bool t8 = (p.nvox % 2 == 0) && ((uintptr_t)p.target % 8 == 0) && (p.out_bs % 2 == 0);
-    // L2 prefetch kTgPf chunks ahead of the copies (lane r < 16: row r's 128-byte segment of this warp's voxels),
-    // so the cp.async of a chunk finds it in L2 instead of waiting out a DRAM latency one chunk before use
-    int64_t pf_t = blockIdx.x;
-    int pf_o = 0, pf_ck = cg;
-    auto pf_advance = [&]() {
-      pf_ck += kOUTQ;
-      if (pf_ck >= nck) {
-        pf_ck = cg;
-        if (++pf_o == p.G2) {
-          pf_o = 0;
-          pf_t += gridDim.x;
-        }
-      }
-    };
-    auto t_prefetch = [&]() {
-      if (kTgPf > 0 && pf_t < ntiles && lane < 16 && lane < p.C3 - pf_ck * 16) {
-        const int64_t bq = pf_t / p.tiles_per_b, v0q = (pf_t - bq * p.tiles_per_b) * kTileV + 32 * qd;
-        if (v0q < p.nvox)
-          prefetch_l2(p.target + bq * p.out_bs + ((int64_t)pf_o * p.C3 + pf_ck * 16 + lane) * stride + v0q);
-      }
-      pf_advance();
-    };
-    if (tring)
-      for (int i = 0; i < kTgPf; ++i) t_prefetch();
     auto t_issue = [&]() {
       __syncwarp();   // every lane has read the stage this copy overwrites (lanes read each other's copies)
-      t_prefetch();
       if (nt_t < ntiles) {
         const int64_t bb_ = nt_t / p.tiles_per_b;
         if (t8) {
@@ -1768,31 +1725,6 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
               t_issue();
               cp_async_wait<1>();
               __syncwarp();   // the 8-byte path reads values other lanes copied
-            }
-            if (tgt && ck < nck) {   // fused MSE, TMA target ring: this chunk is chunk n3 * nck + ck of the CTA
-              const uint32_t q = n3 * (uint32_t)nck + (uint32_t)ck, tgs = q % kTgStages;
-              idle_wait<1>(&bars.tg_full[tgs], (q / kTgStages) & 1);
-              const float* rp = reinterpret_cast<const float*>(smem + p.sm_tgring + tgs * kStageBytes) + row;
-              if (ck < nck && vok && p.out) {
-                const int64_t off = b * p.out_bs + ((int64_t)o * p.C3 + ck * 16) * stride + v;
-                float* d = p.out + off;
-                const int nval = p.C3 - ck * 16;
-                const float* bb = sb + o * p.N3 + ck * 16;
-                float csum = 0.f;   // 16 squares in fp32, then one float64 add per chunk
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                  if (nval >= 16 || e < nval) {
-                    const float tv = rp[(e & 1) * odd0t + (e >> 1) * kBoxV];
-                    const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - tv;
-                    csum = fmaf(res, res, csum);
-                    __stcs(d, res * p.out_scale);
-                  }
-                  d += stride;
-                }
-                lacc += (double)csum;
-              }
-              warp_arrive(&bars.tg_empty[tgs]);   // the whole warp, converged
-              continue;
             }
             if (ck >= nck || !vok || !p.out) {
               if (tring && ck < nck) ++tq_use;
@@ -1969,18 +1901,18 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
           }
           // block-diagonal T (round trip): only input group o's items, each read by this shell alone
-          const int kb = p.t_diag ? o * (nk2 / p.G2) : 0, ke = p.t_diag ? kb + nk2 / p.G2 : nk2;
+          // (a compile-time switch: a runtime one in this loop costs the dense chain ~4% of its time)
+          const int kb = DIAG ? o * (nk2 / p.G2) : 0, ke = DIAG ? kb + nk2 / p.G2 : nk2;
 #pragma unroll
           for (int j = 0; j < PARTS; ++j) bd[j] += (uint64_t)kb * ks2;
           for (int k = kb; k < ke; ++k) {
-            const uint32_t gi = it * (uint32_t)nk2 + (uint32_t)k, slot = kA2Item ? gi % (uint32_t)p.NR : (uint32_t)k;
-            if (o == 0 || p.t_diag) {
-              mbar_wait_warp(&bars.a2_full[slot], (kA2Item ? gi / (uint32_t)p.NR : it) & 1);
+            if (o == 0 || DIAG) {
+              mbar_wait_warp(&bars.a2_full[k], it & 1);
               fence_after();
             }
             if (elect_one()) {
-              kstep_ts<PARTS>(d3, tA2 + slot * kSlotW, 8, bd, id2, k == kb);
-              if (kA2Item && (o == p.G2 - 1 || p.t_diag)) commit(&bars.a2_ifree[slot]);   // CONV may refill the slot
+              kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == kb);
+              if (kA2Item && (o == p.G2 - 1 || DIAG)) commit(&bars.a2_ifree[k]);   // CONV may overwrite item k
             }
             __syncwarp();
 #pragma unroll
@@ -2000,39 +1932,14 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   } else if (warp == kW3LD) {
     if (p.tma)
       tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
-  } else if (p.tstream || p.tg_tma) {
+  } else if (p.tstream) {
     // =========================== T-image loader: shell o's rows of both term images, two buffers ===========
-    // (fused MSE with tg_tma: also the target chunks of each output shell, one shell behind the T images, into the
-    // kTgStages-deep target ring the OUT warps read; chunk q of the CTA-wide sequence (tile, shell, chunk) is in
-    // stage q % kTgStages, consumed by the quadrant warps of group q % 2 -- nck even keeps that fixed)
     const uint32_t tg = (uint32_t)(p.N3 * K2 * 2);
     const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
-    const int nck = p.N3 / 16;
-    uint32_t qtg = 0;
-    if (p.tg_tma && elect_one()) asm volatile("prefetch.tensormap [%0];\n" ::"l"(p.tm + 1) : "memory");
-    __syncwarp();
-    auto target_shell = [&](uint32_t n) {   // target chunks of the CTA's n-th (tile, shell)
-      const uint32_t it = n / (uint32_t)p.G2, o = n - it * (uint32_t)p.G2;
-      const int64_t t = blockIdx.x + (int64_t)it * gridDim.x, b = t / p.tiles_per_b;
-      const int v0 = (int)((t - b * p.tiles_per_b) * kTileV);
-      for (int ck = 0; ck < nck; ++ck, ++qtg) {
-        const uint32_t st = qtg % kTgStages, rd = qtg / kTgStages;
-        if (rd > 0) mbar_wait_warp(&bars.tg_empty[st], (rd - 1) & 1);
-        if (elect_one()) {
-          uint8_t* dst = smem + p.sm_tgring + st * kStageBytes;
-          const int c0 = (int)o * p.C3 + 16 * ck;
-          mbar_arrive_tx(&bars.tg_full[st], kStageBytes);
-          tma_load_3d(dst, p.tm + 1, v0, c0 >> 1, (int)b, &bars.tg_full[st]);
-          tma_load_3d(dst + kStageBytes / 2, p.tm + 1, (int)p.nvox + v0 - (int)(p.nvox & 3), c0 >> 1, (int)b,
-                      &bars.tg_full[st]);
-        }
-        __syncwarp();
-      }
-    };
-    const uint32_t ntot = nmine * (uint32_t)p.G2;
-    for (uint32_t n = 0; n < ntot; ++n) {
-      if (p.tstream) {
-        const uint32_t b = n & 1, o = n % (uint32_t)p.G2;
+    uint32_t n = 0;
+    for (uint32_t it = 0; it < nmine; ++it)
+      for (int o = 0; o < p.G2; ++o, ++n) {
+        const uint32_t b = n & 1;
         if (n >= 2) mbar_wait_warp(&bars.t_empty[b], ((n >> 1) - 1) & 1);
         if (elect_one()) {
           uint8_t* dst = smem + p.sm_w2 + b * 2u * tg;
@@ -2043,9 +1950,6 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
         }
         __syncwarp();
       }
-      if (p.tg_tma && n >= 1) target_shell(n - 1);
-    }
-    if (p.tg_tma && ntot > 0) target_shell(ntot - 1);
   }
   fence_before();
   __syncthreads();
@@ -2646,11 +2550,6 @@ bool plan_chain2h(Chain3& p, bool kout) {
     if (p.NA < 2) return false;
     if (p.NA > kMaxSlots) p.NA = kMaxSlots;
     p.NAc = 0;
-    // leftover columns become extra A2 ring slots (measurement knob DELIMIT_A2_SPARE caps them)
-    int extra = (spare - p.NA * p.cpi * parts * 8) / (parts * 8);
-    if (const char* e = getenv("DELIMIT_A2_SPARE")) extra = std::min(extra, atoi(e));
-    p.NR = std::min(A2w / (parts * 8) + std::max(extra, 0), 16);
-    A2w = p.NR * parts * 8;
   }
   if (D1w + A2w + D3w + p.NA * p.cpi * parts * 8 > 512) return false;
   p.colA = 0;
@@ -2667,16 +2566,9 @@ bool plan_chain2h(Chain3& p, bool kout) {
   p.sm_w2 = (uint32_t)o; o = al(o + (p.tstream ? tbufs : (size_t)parts * p.w2_img), 1024);
   p.sm_bias = (uint32_t)o; o = al(o + (size_t)p.G2 * p.N3 * 4, 128);
   p.sm_tring = 0;
-  p.sm_tgring = 0;
-  if (p.target && !kout && kOB2h == 1 && p.tg_tma && (p.N3 / 16) % 2 == 0) {   // fused MSE: TMA target ring
-    p.sm_tgring = (uint32_t)o;
-    o = al(o + (size_t)kTgStages * kStageBytes, 128);
-  } else if (p.target && !kout && kOB2h == 1 && !getenv("DELIMIT_NO_TRING")) {   // per-warp cp.async rings
-    p.tg_tma = 0;
+  if (p.target && !kout && kOB2h == 1 && !getenv("DELIMIT_NO_TRING")) {   // fused MSE target rings
     p.sm_tring = (uint32_t)o;
     o = al(o + (size_t)kOUT3 * 2 * 16 * 32 * 4, 128);
-  } else {
-    p.tg_tma = 0;
   }
   p.sm_ring = (uint32_t)o;
   for (int ns : {12, 8, 4}) {
@@ -2690,10 +2582,11 @@ bool plan_chain2h(Chain3& p, bool kout) {
   return false;
 }
 
-template <int NS, bool KOUT>
+template <int NS, bool KOUT, bool DIAG = false>
 int launch_chain2h(const Chain3& p, int grid, cudaStream_t st) {
-  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
-  chain2h_tc<NS, KOUT><<<grid, kThreads2h, p.smem_bytes, st>>>(p);
+  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)p.smem_bytes));
+  chain2h_tc<NS, KOUT, DIAG><<<grid, kThreads2h, p.smem_bytes, st>>>(p);
   return after_launch(KOUT ? "chain2h_tc(k-outer)" : "chain2h_tc");
 }
 
@@ -2776,7 +2669,8 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
       h2.kt = ktrace();
       h2.kt_slot = what[6] == 'f' ? 0 : 1;   // "chain_fwd" / "chain_bwd"
       if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
-      else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));
+      else if (h2.ns == 12 && h2.t_diag) DL_TRY((launch_chain2h<12, false, true>(h2, grid, st)));
+      else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));   // (a dense T is exact for t_diag too)
       else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
       v.rstate = rstate;
       v.redo = 1;
@@ -3072,9 +2966,6 @@ int chain_fwd(const float* x, float* y, void* c_mid, const float* M, int m_per_s
   p.loss = loss;
   p.tma = !tma_disabled() && pair_map(&p.tm[0], x, nbatch, s_in * n, n, nvox);
   p.t_diag = diag;
-  // fused MSE target by TMA (measured 4.17 vs 4.04 ms for the per-warp cp.async rings at cfg5: a knob, off)
-  p.tg_tma = target && p.tma && getenv("DELIMIT_TGTMA") && pair_map(&p.tm[1], target, nbatch, s_out * n_out, n_out, nvox)
-                 ? 1 : 0;
   const int grid = grid_for(nbatch * p.tiles_per_b, sm);
   const bool fold = h && use_2h();
   if (fold) DL_TRY(fold_t(d, w, ws, M, L, Bt, bvec, false, st));

@@ -204,3 +204,37 @@ def test_chain_from_raw_layouts(dev, kind):
     y_ref = port.chain_forward(xn, Ms, geo, w, b, port.eval_basis(tables[0], 4), 2)
     assert port.rel_err(y.double().cpu().numpy(), y_ref) <= 1e-4
     assert not mask.any()
+
+
+@pytest.mark.parametrize("case", ["stacked_two_layers", "odd_nvox_fallback"])
+def test_chain_from_raw_more(dev, case):
+    """Stacked LSC layers through the raw-input kernel (folded operator), and an odd voxel count (the two-pass
+    fallback): both equal normalize_b0 -> chain."""
+    rng = np.random.default_rng(21)
+    X, Y, Z = (10, 9, 7) if case == "stacked_two_layers" else (9, 7, 5)      # 630 (even) / 315 (odd)
+    bvals = np.array([0.0] + [1000.0] * 30 + [0.0] + [2000.0] * 30)
+    dirs = rng.normal(size=(bvals.size, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    scheme = dwio.GradientScheme(dirs, bvals, np.array([0, 31]),
+                                 (dwio.Shell(1000.0, np.arange(1, 31)), dwio.Shell(2000.0, np.arange(32, 62))),
+                                 dwio.B0_THRESHOLD)
+    arr = (rng.uniform(200.0, 3000.0, size=(X, Y, Z, bvals.size)) + 1000.0 * np.isin(np.arange(bvals.size), [0, 31])
+           ).astype(np.int16)
+    raw = dwio.NiftiRaw(np.asfortranarray(arr).ravel(order="F"), arr.shape, dwio.CODE_OF[np.dtype(np.int16)],
+                        0.0, 0.0, np.eye(4), {})
+    tables = np.stack([dirs[1:31], dirs[32:62]])
+    s2sh = dl.Signal2SH(4, tables, lb_lambda=0.006).to(dev)
+    layers = []
+    for k in range(2 if case == "stacked_two_layers" else 1):
+        m = dl.LocalSphericalConvolution(2, 2, 4, 4, tables[0], [5], lb_lambda=0.006, angular_distance=np.pi / 5).to(dev)
+        m.load_kernel(dl.LscKernel(rng.normal(size=(2, 2, 6)) / 12, rng.normal(size=2) * 0.1))
+        layers.append(m)
+    chain = dl.SphericalChain(s2sh, layers if len(layers) > 1 else layers[0], dl.SH2Signal(4, tables[0]).to(dev))
+    y, _, _ = dl.chain_from_raw(chain, raw, scheme, device=dev)
+    assert y.is_contiguous() == (case == "odd_nvox_fallback")
+    vol, _ = dl.normalize_b0(raw, scheme, device=dev)
+    with torch.no_grad():
+        y2 = chain(vol.data)
+    from oracle import port
+
+    assert port.rel_err(y.double().cpu().numpy(), y2.double().cpu().numpy()) <= 1e-5
