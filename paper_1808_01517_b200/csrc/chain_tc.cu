@@ -171,6 +171,17 @@ __device__ __forceinline__ void st_cs_u16(uint16_t* p, uint32_t v) {
 // 16 D1 rows of one voxel as their first two bf16 split terms (w0 = hi, w1 = next term, packed row pairs)
 // -> the two term planes of the mid buffer (`plane` halfs apart, rows `pitch` apart).  Row `ones` (or -1)
 // is stored as exactly 1.0: a zero-weight padding row whose Gram column sums g (the bias gradient).
+// row `ones` (0..15; anything else: none) of a lane's packed term words becomes the bias column (1.0, 0)
+__device__ __forceinline__ void set_ones(uint32_t (&w0)[8], uint32_t (&w1)[8], int ones) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (2 * i == ones) { w0[i] = (w0[i] & 0xFFFF0000u) | 0x3F80u; w1[i] &= 0xFFFF0000u; }
+    if (2 * i + 1 == ones) { w0[i] = (w0[i] & 0x0000FFFFu) | 0x3F800000u; w1[i] &= 0x0000FFFFu; }
+  }
+}
+
+// ONES = false: the caller has applied set_ones already (or the item has no bias row)
+template <bool ONES = true>
 __device__ __forceinline__ void store_mid(uint16_t* d, int64_t plane, int64_t pitch, const uint32_t (&w0)[8],
                                           const uint32_t (&w1)[8], int ones) {
   // Lanes (2j, 2j+1) hold adjacent voxels: they trade their packed row pairs so that the even lane stores
@@ -181,8 +192,8 @@ __device__ __forceinline__ void store_mid(uint16_t* d, int64_t plane, int64_t pi
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     uint32_t a = w0[i], c = w1[i];
-    if (2 * i == ones) { a = (a & 0xFFFF0000u) | 0x3F80u; c &= 0xFFFF0000u; }
-    if (2 * i + 1 == ones) { a = (a & 0x0000FFFFu) | 0x3F800000u; c &= 0x0000FFFFu; }
+    if (ONES && 2 * i == ones) { a = (a & 0xFFFF0000u) | 0x3F80u; c &= 0xFFFF0000u; }
+    if (ONES && 2 * i + 1 == ones) { a = (a & 0x0000FFFFu) | 0x3F800000u; c &= 0x0000FFFFu; }
     const uint32_t pa = __shfl_xor_sync(0xffffffffu, a, 1), pc = __shfl_xor_sync(0xffffffffu, c, 1);
     const uint32_t sel_lo = odd ? 0x7632u : 0x5410u;
     const uint32_t wa = odd ? __byte_perm(pa, a, sel_lo) : __byte_perm(a, pa, sel_lo);
@@ -519,15 +530,26 @@ __device__ __forceinline__ void in_role_tma2(const Geo& geo, int per_tile, int64
       }
 #else
       float v0[16], v1[16];
-      idle_wait<0>(&full[cs0], (q0 / NS) & 1);
-      const float* rp0 = ring + cs0 * (kStageBytes / 4) + 32 * qd + lane;
+      // a full chunk (every row valid) reads without per-row predicates: two row bases, immediate offsets
+      auto ld_chunk = [&](float (&v)[16], const float* rp, int nv) {
+        if (nv >= 16) {
+          const float* re = rp;
+          const float* ro = rp + odd0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v0[j] = j < nval0 ? rp0[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+          for (int j = 0; j < 16; j += 2) {
+            v[j] = re[(j >> 1) * kBoxV];
+            v[j + 1] = ro[(j >> 1) * kBoxV];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = j < nv ? rp[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+        }
+      };
+      idle_wait<0>(&full[cs0], (q0 / NS) & 1);
+      ld_chunk(v0, ring + cs0 * (kStageBytes / 4) + 32 * qd + lane, nval0);
       warp_arrive(&empty[cs0]);
       idle_wait<0>(&full[cs1], ((q0 + 1) / NS) & 1);
-      const float* rp1 = ring + cs1 * (kStageBytes / 4) + 32 * qd + lane;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v1[j] = j < nval1 ? rp1[(j & 1) * odd0 + (j >> 1) * kBoxV] : 0.f;
+      ld_chunk(v1, ring + cs1 * (kStageBytes / 4) + 32 * qd + lane, nval1);
       warp_arrive(&empty[cs1]);
       scale16<H>(v0, sc, am);
       scale16<H>(v1, sc, am);
@@ -1562,6 +1584,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     const int cw = (warp - kIN3) >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
     const int n1c = p.N1 / 16;
+    const int ones_item = p.mid_ones >= 0 ? p.mid_ones >> 4 : -1;   // the item holding c's bias row
     uint32_t gq = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t b = t / p.tiles_per_b, vx = (t - b * p.tiles_per_b) * kTileV + 32 * (warp & 3) + lane;
@@ -1619,7 +1642,8 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
             for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
             uint32_t m[2][8];
             split16<2>(u, m);
-            store_mid(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
+            if (i == ones_item) set_ones(m[0], m[1], vok ? p.mid_ones - 16 * i : -1);   // only the bias row's item
+            store_mid<false>(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], -1);
           }
         }
         fence_before();
@@ -1770,10 +1794,25 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
                 }
               }
               lacc += (double)csum;
+            } else if (nval >= 16) {
+              // full chunk: no per-row predicate, one 128-bit bias load per four rows, and the row pointer
+              // bumped by a 32-bit byte stride (the predicated form costs ~8 instructions per row)
+              const uint32_t rs = (uint32_t)stride * 4u;
+              char* dc = reinterpret_cast<char*>(d);
+#pragma unroll
+              for (int h = 0; h < 16; h += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(bb + h);
+                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  __stcs(reinterpret_cast<float*>(dc), fmaf(__uint_as_float(r[k][h + e]), isc, bv[e]));
+                  dc += rs;
+                }
+              }
             } else {
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                if (nval >= 16 || e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
+                if (e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
                 d += stride;
               }
             }
@@ -2531,7 +2570,9 @@ bool use_2h() {
 // stage-1 image | folded T images | folded bias | TMA ring (a multiple of 4 deep) | barriers.
 bool plan_chain2h(Chain3& p, bool kout) {
   constexpr int parts = 2;
+  // (nvox < 2^30: the OUT role steps between output rows by a 32-bit byte stride)
   if ((!p.tma && !p.raw) || p.N1 > 256 || p.N3 > 256 || (p.G1 * p.N1) / 16 > 16 || (p.K1 / 16) % 2 ||
+      p.nvox >= (1LL << 30) ||
       (kout && (p.G2 > 4 || p.raw)))
     return false;
   const int D1w = (p.G1 >= 2 ? 2 : 1) * p.N1;
