@@ -1684,11 +1684,22 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           const uint32_t nb = vv + 1 < p.nvox ? 8u : vv < p.nvox ? 4u : 0u;
           const float* src = p.target + bb_ * p.out_bs + ((int64_t)nt_o * p.C3 + nt_ck * 16) * stride + (nb ? vv : 0);
           float* dst = tr + (tq_issue & 1) * 512 + pv;
+          if (nrow >= 16 && nb == 8u) {   // full chunk, both voxels inside: a 32-bit byte stride per row pair
+            const char* sp = reinterpret_cast<const char*>(src + (lane >> 4) * stride);
+            const uint32_t rs2 = (uint32_t)stride * 8u;
+            float* dp = dst + (lane >> 4) * 32;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = 2 * i + (lane >> 4);
-            const bool ok = r < nrow && nb;
-            cp_async8(dst + r * 32, ok ? src + (int64_t)r * stride : p.target, ok ? nb : 0u);
+            for (int i = 0; i < 8; ++i) {
+              cp_async8(dp + 2 * i * 32, reinterpret_cast<const float*>(sp), 8u);
+              sp += rs2;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 2 * i + (lane >> 4);
+              const bool ok = r < nrow && nb;
+              cp_async8(dst + r * 32, ok ? src + (int64_t)r * stride : p.target, ok ? nb : 0u);
+            }
           }
         } else {
           const int64_t vv = (nt_t - bb_ * p.tiles_per_b) * kTileV + row;
@@ -1762,14 +1773,31 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
               const float* tv = tr + (tq_use & 1) * 512 + lane;
               ++tq_use;
               float csum = 0.f;   // 16 squares in fp32, then one float64 add per chunk
+              if (nval >= 16) {   // full chunk: as the plain path below
+                const uint32_t rs = (uint32_t)stride * 4u;
+                char* dc = reinterpret_cast<char*>(d);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                if (nval >= 16 || e < nval) {
-                  const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - tv[e * 32];
-                  csum = fmaf(res, res, csum);
-                  __stcs(d, res * p.out_scale);
+                for (int h = 0; h < 16; h += 4) {
+                  const float4 b4 = *reinterpret_cast<const float4*>(bb + h);
+                  const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float res = fmaf(__uint_as_float(r[k][h + e]), isc, bv[e]) - tv[(h + e) * 32];
+                    csum = fmaf(res, res, csum);
+                    __stcs(reinterpret_cast<float*>(dc), res * p.out_scale);
+                    dc += rs;
+                  }
                 }
-                d += stride;
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  if (e < nval) {
+                    const float res = fmaf(__uint_as_float(r[k][e]), isc, bb[e]) - tv[e * 32];
+                    csum = fmaf(res, res, csum);
+                    __stcs(d, res * p.out_scale);
+                  }
+                  d += stride;
+                }
               }
               lacc += (double)csum;
             } else if (p.target) {   // fused MSE: d(loss)/dy, and the squared residuals
