@@ -1,10 +1,15 @@
-# round 2 measurement batch: GPU suite, smoke, every bench config, launch list + full capture of the default command
+# round 2 measurement batch: GPU suite, smoke, every bench config, the reference arm, launch list + full ncu
+# capture of the chain kernels (each ncu command after the same command exited 0 without ncu)
 set -x
 timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -4
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-for c in cfg4 cfg2 cfg5 cfg3 cfg1; do
+python bench.py --steps 20 --warmup 5 > gpurun_out/fin_plain.json 2> gpurun_out/fin_plain.err; echo "plain rc=$?"
+for c in cfg2 cfg5 cfg3 cfg1; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/fin_$c.json 2> gpurun_out/fin_$c.err; echo "$c rc=$?"
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/fin_ref.json 2>&1; echo "ref rc=$?"
-python bench.py --steps 20 --warmup 5 > gpurun_out/fin_plain.json 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 420 --csv --log-file gpurun_out/fin_launches.csv python bench.py --steps 20 --warmup 5 > gpurun_out/fin_ncu.log 2>&1; echo "ncu rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 420 --csv --log-file gpurun_out/fin_launches.csv python bench.py --steps 20 --warmup 5 > gpurun_out/fin_ncu.log 2>&1; echo "ncu launches rc=$?"
+timeout 300 python scripts/ncu_chain.py 3 && echo chain ok
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:chain2h|gram_tc" -s 3 -c 3 -f -o gpurun_out/fin_chain python scripts/ncu_chain.py 3 > gpurun_out/fin_ncu_chain.log 2>&1; echo "ncu chain rc=$?"
+timeout 300 python scripts/ncu_chain.py 3 cfg5 && echo mse ok
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:chain2h -s 2 -c 1 -f -o gpurun_out/fin_mse python scripts/ncu_chain.py 3 cfg5 > gpurun_out/fin_ncu_mse.log 2>&1; echo "ncu mse rc=$?"

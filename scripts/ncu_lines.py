@@ -11,6 +11,7 @@ opcode mix of the wait instructions.
 """
 import collections
 import csv
+import os
 import re
 import sys
 
@@ -77,7 +78,7 @@ def main():
     print(f"instructions {tot_e:.4g}, stall samples {tot_s:.0f}")
     for title, key in (("by instructions executed", 0), ("by stall samples", 1)):
         print(f"--- top lines {title}")
-        for line, d in sorted(per_line.items(), key=lambda kv: -kv[1][key])[:28]:
+        for line, d in sorted(per_line.items(), key=lambda kv: -kv[1][key])[:int(os.environ.get("NCU_LINES_TOP", 28))]:
             ops = ", ".join(f"{o} {c / max(d[0], 1) * 100:.0f}%" for o, c in d[2].most_common(4))
             code = src[line - 1].strip()[:70] if (src and line) else ""
             print(f"{str(line):>6} instr {d[0] / tot_e * 100:5.1f}%  samples {d[1] / tot_s * 100:5.1f}%  [{ops}]  {code}")
