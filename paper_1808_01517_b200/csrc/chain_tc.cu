@@ -1085,8 +1085,9 @@ __global__ void __launch_bounds__(kThreads3, 1) chain3v_tc(const __grid_constant
   const int64_t ntiles = p.nbatch * p.tiles_per_b;
   const int nk1 = p.K1 / 16, per_tile = p.G1 * nk1;
   const int K2 = p.G1 * p.N1, nk2 = K2 / 16, nk3 = p.N2 / 16;
+  const float inv_nk1 = 1.f / (float)nk1;   // r / nk1 without an integer division (r < 256: exact)
   auto geo = [&](int r) {
-    const int g = r / nk1, k = r - g * nk1;
+    const int g = (int)(((float)r + 0.5f) * inv_nk1), k = r - g * nk1;
     return ChunkGeo{0, g * p.C1 + 16 * k, p.C1 - 16 * k};
   };
 
@@ -1837,11 +1838,18 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
                   dc += rs;
                 }
               }
-            } else {
+            } else {   // the shell's last, partial chunk: the same addressing, rows predicated
+              const uint32_t rs = (uint32_t)stride * 4u;
+              char* dc = reinterpret_cast<char*>(d);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                if (e < nval) __stcs(d, fmaf(__uint_as_float(r[k][e]), isc, bb[e]));
-                d += stride;
+              for (int h = 0; h < 16; h += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(bb + h);   // bias rows are padded to N3
+                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  if (h + e < nval) __stcs(reinterpret_cast<float*>(dc), fmaf(__uint_as_float(r[k][h + e]), isc, bv[e]));
+                  dc += rs;
+                }
               }
             }
           }
