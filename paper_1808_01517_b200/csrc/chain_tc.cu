@@ -1456,6 +1456,12 @@ constexpr bool kA2Item = DL_A2_ITEM != 0;
 #define DL_MID_LATE 1
 #endif
 constexpr bool kMidLate = DL_MID_LATE != 0;
+// stage 2: shells 0 and 1 of a tile interleaved so that their last kDefer items come after both shells' other
+// items (0: shell after shell)
+#ifndef DL_DEFER
+#define DL_DEFER 1
+#endif
+constexpr int kDefer = DL_DEFER;
 // chain2h keeps its barriers small: with the 12-deep TMA ring the shared-memory plan has < 900 bytes left for
 // them (a larger block silently drops the ring to 8 stages)
 constexpr int kMaxStages2h = 12;
@@ -1955,52 +1961,74 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
         }
       } else
       for (uint32_t it = 0; it < nmine; ++it) {
-        uint64_t bg[PARTS];
-#pragma unroll
-        for (int j = 0; j < PARTS; ++j) bg[j] = B2[j];
-        for (int o = 0; o < p.G2; ++o, ++n3) {
-          const uint32_t xb = n3 & 1;
-          if (n3 >= 2) {
-            mbar_wait_warp(&bars.d3_free[xb], ((n3 >> 1) - 1) & 1);
+        const uint32_t n3b = it * (uint32_t)p.G2;   // the CTA-wide index of this tile's shell 0
+        // shell o: wait for its D3 buffer (and T image), return the buffer; bd = its T descriptors at item 0
+        auto shell_begin = [&](int o, uint64_t (&bd)[PARTS]) -> uint32_t {
+          const uint32_t n = n3b + (uint32_t)o, xb = n & 1;
+          if (n >= 2) {
+            mbar_wait_warp(&bars.d3_free[xb], ((n >> 1) - 1) & 1);
             fence_after();
           }
-          const uint32_t d3 = tD3 + xb * (uint32_t)p.N3;
-          uint64_t bd[PARTS];
-          if (p.tstream) {   // this shell's T image in buffer n3 & 1 (rows 0.. of the buffer)
-            mbar_wait_warp(&bars.t_full[xb], (n3 >> 1) & 1);
+          if (p.tstream) {   // this shell's T image in buffer n & 1 (rows 0.. of the buffer)
+            mbar_wait_warp(&bars.t_full[xb], (n >> 1) & 1);
 #pragma unroll
             for (int j = 0; j < PARTS; ++j)
               bd[j] = wdesc(sw2 + xb * (uint32_t)PARTS * tg + (uint32_t)j * tg, K2, 1, 0);
           } else {
 #pragma unroll
-            for (int j = 0; j < PARTS; ++j) bd[j] = bg[j];
+            for (int j = 0; j < PARTS; ++j) bd[j] = B2[j] + (uint64_t)o * o2s;
           }
-          // block-diagonal T (round trip): only input group o's items, each read by this shell alone
-          // (a compile-time switch: a runtime one in this loop costs the dense chain ~4% of its time)
-          const int kb = DIAG ? o * (nk2 / p.G2) : 0, ke = DIAG ? kb + nk2 / p.G2 : nk2;
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) bd[j] += (uint64_t)kb * ks2;
-          for (int k = kb; k < ke; ++k) {
-            if (o == 0 || DIAG) {
+          return tD3 + xb * (uint32_t)p.N3;
+        };
+        // items k0..k1-1 of shell o into d3 (k == kfirst overwrites the accumulator)
+        auto run_items = [&](int o, uint32_t d3, const uint64_t (&bd)[PARTS], int k0, int k1, int kfirst) {
+          for (int k = k0; k < k1; ++k) {
+            if (o == 0 || DIAG) {   // the item's first reader in this tile
               mbar_wait_warp(&bars.a2_full[k], it & 1);
               fence_after();
             }
             if (elect_one()) {
-              kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bd, id2, k == kb);
+              uint64_t bk[PARTS];
+#pragma unroll
+              for (int j = 0; j < PARTS; ++j) bk[j] = bd[j] + (uint64_t)k * ks2;
+              kstep_ts<PARTS>(d3, tA2 + (uint32_t)k * kSlotW, 8, bk, id2, k == kfirst);
               if (kA2Item && (o == p.G2 - 1 || DIAG)) commit(&bars.a2_ifree[k]);   // CONV may overwrite item k
             }
             __syncwarp();
-#pragma unroll
-            for (int j = 0; j < PARTS; ++j) bd[j] += ks2;
           }
+        };
+        auto shell_end = [&](int o) {
+          const uint32_t xb = (n3b + (uint32_t)o) & 1;
           if (elect_one()) {
             commit(&bars.d3_full[xb]);
             if (p.tstream) commit(&bars.t_empty[xb]);
             if (!kA2Item && o == p.G2 - 1) commit(&bars.a2_free);
           }
           __syncwarp();
-#pragma unroll
-          for (int j = 0; j < PARTS; ++j) bg[j] += o2s;
+        };
+        int o = 0;
+        if (!DIAG && kDefer > 0 && p.G2 >= 2 && nk2 > kDefer) {
+          // shells 0 and 1 interleaved: both run their first nk2 - kDefer items before either reads the last
+          // ones, so the items the previous tile's last shell frees last have twice the slack to be refilled
+          uint64_t b0[PARTS], b1[PARTS];
+          const uint32_t d0 = shell_begin(0, b0);
+          run_items(0, d0, b0, 0, nk2 - kDefer, 0);
+          const uint32_t d1 = shell_begin(1, b1);
+          run_items(1, d1, b1, 0, nk2 - kDefer, 0);
+          run_items(0, d0, b0, nk2 - kDefer, nk2, 0);
+          shell_end(0);
+          run_items(1, d1, b1, nk2 - kDefer, nk2, 0);
+          shell_end(1);
+          o = 2;
+        }
+        for (; o < p.G2; ++o) {
+          uint64_t bd[PARTS];
+          const uint32_t d3 = shell_begin(o, bd);
+          // block-diagonal T (round trip): only input group o's items, each read by this shell alone
+          // (a compile-time switch: a runtime one in this loop costs the dense chain ~4% of its time)
+          const int kb = DIAG ? o * (nk2 / p.G2) : 0, ke = DIAG ? kb + nk2 / p.G2 : nk2;
+          run_items(o, d3, bd, kb, ke, kb);
+          shell_end(o);
         }
       }
     }
