@@ -1484,7 +1484,9 @@ constexpr int kThreads2h = (kWT + 1) * 32;
 // KOUT = true: A2 items stream through a ring (NAc slots) and stage 2 is K-outer over all output shells
 //   (D3 holds every shell; OUT releases shell o as soon as it is drained, so the next tile's first K-step
 //   into shell o can start), which removes the CONV -> stage 2 -> a2_free -> CONV cycle of the tile.
-template <int NS, bool KOUT, bool DIAG>
+// GONLY: a g-only adjoint (no dx requested: the first layer of a training step): stage 1 and the Gram term planes
+// only -- no A2, no stage 2, no OUT stores, no T images.
+template <int NS, bool KOUT, bool DIAG, bool GONLY>
 __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constant__ Chain3 p) {
   constexpr int PARTS = 2;
   constexpr bool H = true;
@@ -1612,6 +1614,18 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           float v[16];
           ld16f(tq + p.colD1 + buf * (uint32_t)p.N1 + (uint32_t)c * 16, v);
           track16<H>(v, amax);
+          if constexpr (GONLY) {   // the Gram term planes are the only product
+            if (mid) {
+              float u[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) u[e] = v[e] * isc;
+              uint32_t m[2][8];
+              split16<2>(u, m);
+              if (i == ones_item) set_ones(m[0], m[1], vok ? p.mid_ones - 16 * i : -1);
+              store_mid<false>(mid + (int64_t)i * 16 * 64, (int64_t)K2 * 64, 64, m[0], m[1], -1);
+            }
+            continue;
+          }
           uint32_t w[PARTS][8];
           split16<PARTS, H>(v, w);
           if (mid && !kMidLate) {
@@ -1659,6 +1673,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     }
     amax_publish(p.rstate + kStAmaxMid, amax);
   } else if (warp < kW3MMA) {
+    if constexpr (!GONLY) {
     // =========================== OUT: D3 -> HBM (x 2^-e + folded bias) ===========================
     const int ow = warp - kIN3 - kCV3, qd = warp & 3, cg = ow >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * qd) << 16);
@@ -1864,6 +1879,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
     }
     if (tring) cp_async_wait<0>();
     if (p.target) loss_publish(p.loss, lacc);
+    }
   } else if (warp == kW3MMA || warp == kW3MMA2) {
     // =========================== MMA issuers ===========================
     const uint32_t sw1 = smem_u32(smem + p.sm_w1), sw2 = smem_u32(smem + p.sm_w2);
@@ -1918,7 +1934,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
           }
         }
       }
-    } else {
+    } else if constexpr (!GONLY) {
       // stage 2: T_o images, part-major (term j of group o at j * w2_img, group o rows o * N3 .. of a G2*N3 x K2 image)
       uint64_t B2[PARTS];
 #pragma unroll
@@ -2035,7 +2051,7 @@ __global__ void __launch_bounds__(kThreads2h, 1) chain2h_tc(const __grid_constan
   } else if (warp == kW3LD) {
     if (p.tma)
       tma_loader<NS>(geo, per_tile, ntiles, p.tiles_per_b, p.nvox, p.tm, smem + p.sm_ring, bars.full, bars.empty);
-  } else if (p.tstream) {
+  } else if (!GONLY && p.tstream) {
     // =========================== T-image loader: shell o's rows of both term images, two buffers ===========
     const uint32_t tg = (uint32_t)(p.N3 * K2 * 2);
     const uint32_t nmine = ntiles > (int64_t)blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
@@ -2687,11 +2703,11 @@ bool plan_chain2h(Chain3& p, bool kout) {
   return false;
 }
 
-template <int NS, bool KOUT, bool DIAG = false>
+template <int NS, bool KOUT, bool DIAG = false, bool GONLY = false>
 int launch_chain2h(const Chain3& p, int grid, cudaStream_t st) {
-  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DL_CUDA(cudaFuncSetAttribute(chain2h_tc<NS, KOUT, DIAG, GONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)p.smem_bytes));
-  chain2h_tc<NS, KOUT, DIAG><<<grid, kThreads2h, p.smem_bytes, st>>>(p);
+  chain2h_tc<NS, KOUT, DIAG, GONLY><<<grid, kThreads2h, p.smem_bytes, st>>>(p);
   return after_launch(KOUT ? "chain2h_tc(k-outer)" : "chain2h_tc");
 }
 
@@ -2775,6 +2791,8 @@ int run_chain(Chain3 p, const Dims& d, int grid, cudaStream_t st, const char* wh
       h2.kt_slot = what[6] == 'f' ? 0 : 1;   // "chain_fwd" / "chain_bwd"
       if (kout) DL_TRY((h2.ns == 8 ? launch_chain2h<8, true>(h2, grid, st) : launch_chain2h<4, true>(h2, grid, st)));
       else if (h2.ns == 12 && h2.t_diag) DL_TRY((launch_chain2h<12, false, true>(h2, grid, st)));
+      else if (h2.ns == 12 && !h2.out && h2.mid && !h2.target)   // g-only adjoint
+        DL_TRY((launch_chain2h<12, false, false, true>(h2, grid, st)));
       else if (h2.ns == 12) DL_TRY((launch_chain2h<12, false>(h2, grid, st)));   // (a dense T is exact for t_diag too)
       else DL_TRY((h2.ns == 8 ? launch_chain2h<8, false>(h2, grid, st) : launch_chain2h<4, false>(h2, grid, st)));
       v.rstate = rstate;
