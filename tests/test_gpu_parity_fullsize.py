@@ -13,6 +13,8 @@ Every voxel of every output is compared, not a sample:
 * cfg2 -- Signal2SH -> SH2Signal round trip on the same volume, fwd + bwd, fp64 torch.
 * cfg3 -- LocalSphericalConvolution 1->1 on (4, 45, 32, 32, 32), fwd + bwd, vs the port.
 * cfg1 -- Signal2SH on (1, 90, 32, 32, 32) vs the port.
+* cfg5 -- one subject of the training step (2 stacked LSC layers, fused MSE, g-only adjoint): the loss and
+  every layer's dW / db over every voxel, float64.
 
 Tolerances (north_star): normwise max|got - ref| / max|ref| <= 1e-5 for SH coefficients and
 signals (cfg1, cfg2), <= 1e-4 for LSC outputs and all LSC-chain gradients (cfg3, cfg4).
@@ -270,3 +272,70 @@ def test_cfg1_signal2sh_32cubed_vs_port(dev):
     e_dx = port.rel_err(N(xt.grad), port.signal_to_sh_adjoint(dc, M, 1))
     print(f"cfg1 rel err: c {e_c:.2e} dx {e_dx:.2e} (tolerance {TOL_SH:g})")
     assert e_c <= TOL_SH and e_dx <= TOL_SH
+
+
+@pytest.mark.gpu
+def test_cfg5_hcp_two_layer_mse_step_full_volume(dev):
+    """cfg5's training step on one HCP subject: Signal2SH -> 2 x LSC 3->3 -> SH2Signal, the MSE loss fused into the
+    forward kernel and an input that needs no gradient (the g-only adjoint: stage 1 and the Gram planes only).
+    The loss and every layer's dW / db over all 3,658,350 voxels against float64."""
+    d = unit_sphere_directions(NDIR)
+    rng = np.random.default_rng(7)
+    ws = [rng.normal(size=(3, 3, 6)) / 18.0 for _ in range(2)]
+    bs = [rng.normal(size=3) * 0.1 for _ in range(2)]
+    s2sh = dl.Signal2SH(ORDER, d, lb_lambda=LAM).to(dev)
+    lscs = []
+    for w, b in zip(ws, bs):
+        m = dl.LocalSphericalConvolution(3, 3, ORDER, ORDER, d, [5], lb_lambda=LAM, angular_distance=np.pi / 5).to(dev)
+        m.load_kernel(dl.LscKernel(w, b))
+        lscs.append(m)
+    sh2s = dl.SH2Signal(ORDER, d).to(dev)
+    net = dl.SphericalChain(s2sh, lscs, sh2s)
+    assert net.fused()
+    x, _ = hcp_inputs(dev, 2000)
+    t, _ = hcp_inputs(dev, 3000)
+    for _ in range(2):   # the second call runs with the delayed-scaling state the first one left
+        for m in lscs:
+            m.zero_grad(set_to_none=True)
+        loss = net.mse_loss(x, t)
+        loss.backward()
+    torch.cuda.synchronize()
+    wq = [N(m.sconv.weight)[:, :, 0, :] for m in lscs]
+    bq = [N(m.sconv.bias) for m in lscs]
+    ops = [chain_operators(d, w, b) for w, b in zip(wq, bq)]
+    td = lambda a: torch.tensor(a, dtype=torch.float64, device=dev)   # noqa: E731
+    M, Bt, beta, P = ops[0]["M"], ops[0]["Bt"], td(ops[0]["beta"]), td(ops[0]["P"])
+    K, R = P.shape[0], M.shape[0]
+    L = [td(np.einsum("osk,krt->orst", w, ops[0]["P"]).reshape(3 * R, 3 * R)) for w in wq]
+    bias = [td(np.kron(b, ops[0]["beta"]))[:, None] for b in bq]
+    Mb, Bb = td(np.kron(np.eye(3), M)), td(np.kron(np.eye(3), Bt))
+    V = int(np.prod(HCP))
+    X, TT = x.view(270, V), t.view(270, V)
+    nel = 270.0 * V
+    sq = 0.0
+    G2 = torch.zeros((135, 135), dtype=torch.float64, device=dev)
+    G1 = torch.zeros((135, 135), dtype=torch.float64, device=dev)
+    s2 = torch.zeros(135, dtype=torch.float64, device=dev)
+    s1 = torch.zeros(135, dtype=torch.float64, device=dev)
+    for lo in range(0, V, CHUNK):
+        hi = min(V, lo + CHUNK)
+        c = Mb @ X[:, lo:hi].double()
+        u1 = L[0] @ c + bias[0]
+        u2 = L[1] @ u1 + bias[1]
+        r = Bb @ u2 - TT[:, lo:hi].double()
+        sq += float((r * r).sum())
+        g2 = Bb.T @ (2.0 * r / nel)
+        g1 = L[1].T @ g2
+        G2 += g2 @ u1.T
+        G1 += g1 @ c.T
+        s2 += g2.sum(dim=1)
+        s1 += g1.sum(dim=1)
+    e_loss = abs(float(loss.detach()) - sq / nel) / (sq / nel)
+    errs = [e_loss]
+    for m, G, gs in ((lscs[0], G1, s1), (lscs[1], G2, s2)):
+        dW_ref = torch.einsum("krt,orst->osk", P, G.view(3, R, 3, R))
+        db_ref = gs.view(3, R) @ beta
+        errs += [port.rel_err(N(m.sconv.weight.grad)[:, :, 0, :], N(dW_ref)), port.rel_err(N(m.sconv.bias.grad), N(db_ref))]
+    print("cfg5 one-subject step rel err: loss {:.2e} dW1 {:.2e} db1 {:.2e} dW2 {:.2e} db2 {:.2e}".format(*errs))
+    assert e_loss <= TOL_SH
+    assert max(errs[1:]) <= TOL_LSC
